@@ -1,0 +1,129 @@
+/*
+ * yy.h — C ABI of the B200-native Yin-Yang AC direction-splitting time step
+ * (Takhirov, Frolov & Minev, arXiv 1905.02300).
+ *
+ * One context = one spherical shell R1 <= r <= R2 covered by the two Yin-Yang
+ * patches (§2), each a MAC grid of nr x ntheta x nphi cells
+ * (PAPER.md L473-475).  yy_step advances the Navier-Stokes-Boussinesq system
+ * (eq:eq_ns, eq:eq_heat_convec) by the second-order
+ * artificial-compressibility direction-splitting scheme (§3, eq:Convect_Douglas,
+ * eq:r_comp, eq:theta_comp, eq:phi_comp, eq:nst_Mass1, eq:ac2) with additive
+ * Schwarz iteration between the patches and the splitting-error reduction of
+ * eq:er (§4), iterated until the successive-iterate l2 difference
+ * is below the tolerance (§5.1).  Readings of garbled passages:
+ * DESIGN.md (RD1-RD42 of SURVEY.md §8(c)).
+ *
+ * Geometry (reading RD1/RD2): per patch theta in [pi/4 - d, 3pi/4 + d],
+ * phi in [-3pi/4 - d, 3pi/4 + d], d = 2 theta-cells, dtheta = pi/(2(ntheta-4)),
+ * dphi = (3pi/2 + 2d)/nphi, dr = (R2-R1)/nr.  Patch 0 = Yin, 1 = Yang.
+ *
+ * Array layout (host and device): C order, fp64, phi fastest.  Spherical
+ * vector components are in the patch's own chart basis.
+ *     u_r   (nr+1, ntheta,   nphi)      r-faces
+ *     u_th  (nr,   ntheta+1, nphi)      theta-faces
+ *     u_ph  (nr,   ntheta,   nphi+1)    phi-faces
+ *     p, T  (nr,   ntheta,   nphi)      cell centres
+ * The outermost theta/phi node layer of every array is the Schwarz fringe
+ * (reading RD3): values there are Dirichlet data overwritten by interpolation
+ * from the other patch every iteration; u_r planes 0 and nr are the walls.
+ *
+ * Ownership: host pointers are borrowed for the duration of a call; set/get
+ * are synchronous with respect to the host.  The context owns every device
+ * buffer.  Errors: negative status = failure (see yy_last_error); YY_ENOCONV
+ * is a positive warning (state advanced, some step hit max_iters).  After
+ * YY_ECUDA the only valid call is yy_destroy.  One context per host thread.
+ */
+#ifndef YY_H
+#define YY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  YY_OK = 0,
+  YY_ENOCONV = 4,   /* warning: a step stopped at max_iters (SPEC exit 4)       */
+  YY_EINVAL = -2,   /* argument validation (SPEC exit 2)                          */
+  YY_ESOLVER = -3,  /* NaN/Inf residual (SPEC exit 3)                             */
+  YY_ECUDA = -10,
+  YY_ENCCL = -11,
+  YY_ENOMEM = -12,
+  YY_ESTATE = -13
+} yy_status;
+
+/* time basis of wall data / sources: value(t) = sum_m g_m(t) * term_m */
+enum { YY_TF_ONE = 0, YY_TF_COS = 1, YY_TF_SIN = 2, YY_TF_COS2 = 3 };
+
+/* yy_set_param keys */
+enum {
+  YY_CHI = 1,          /* artificial-compressibility chi (eq:ac1); default 1 (RD19) */
+  YY_MAX_ITERS = 2,    /* Schwarz K_max (RD25); default 100                                  */
+  YY_FIXED_ITERS = 3   /* >0: run exactly this many iterations per step, ignore tol          */
+};
+
+typedef struct {
+  int32_t nr, ntheta, nphi;   /* cells per patch; ntheta >= 8, nphi >= 8, nr >= 2 */
+} yy_grid;
+
+typedef struct yy_ctx yy_ctx;
+
+/* Host pointers to one patch's fields (shapes above).  A NULL member means
+ * "leave unchanged" (set) or "do not copy" (get). */
+typedef struct {
+  double *ur, *ut, *up, *p, *T;
+} yy_fields;
+
+/* Create a context on the current CUDA device.  R1 < R2 radii, Pr Prandtl
+ * number (momentum viscosity nu = Pr, RD33), Ra Rayleigh number (buoyancy
+ * +Pr*Ra*T e_r, RD20), dt > 0 time step.  All state starts at zero, t = 0. */
+yy_status yy_create(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
+                    yy_ctx** out);
+
+/* Set one patch's state.  level 0 = t^n, 1 = t^{n-1} (p ignored).  system
+ * 0 = both bootstrapped systems (u1 = u2, p1 = p2; eq:ac1/eq:ac2), 1 or 2 =
+ * that system only.  T is shared by both systems. */
+yy_status yy_set_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system,
+                        const yy_fields* f);
+
+/* Copy one patch's state to the host (system 1 or 2; 2 is the second-order answer). */
+yy_status yy_get_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system,
+                        yy_fields* out);
+
+/* Wall (r = R1, R2) Dirichlet data of one patch as nterms <= 4 time-basis
+ * terms.  terms[m].T / .ur are (2, ntheta, nphi), .ut (2, ntheta+1, nphi),
+ * .up (2, ntheta, nphi+1) — index 0 = inner wall; NULL member = zero; .p unused.
+ * Default: homogeneous walls (eq:eq_ns, eq:eq_heat_convec). */
+yy_status yy_set_wall(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t* timefn,
+                      const yy_fields* terms);
+
+/* Volume sources (manufactured forcing, reading RD32) as nterms <= 4 terms,
+ * full 3-D staggered arrays; evaluated at t_{n+1/2}; .p unused. */
+yy_status yy_set_source(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t* timefn,
+                        const yy_fields* terms);
+
+yy_status yy_set_param(yy_ctx* ctx, int32_t key, double value);
+
+/* Launch every kernel on this stream (a cudaStream_t, e.g.
+ * torch.cuda.current_stream().cuda_stream).  Default: the legacy stream. */
+yy_status yy_set_stream(yy_ctx* ctx, void* cuda_stream);
+
+/* Advance nsteps time steps; each step iterates Schwarz until
+ * rho_k < schwarz_tol (or max_iters / fixed_iters). */
+yy_status yy_step(yy_ctx* ctx, int32_t nsteps, double schwarz_tol);
+
+/* Per-step Schwarz iteration counts and final rho of every step taken so far
+ * (up to cap entries, most recent last); *n_out = number written. */
+yy_status yy_get_stats(const yy_ctx* ctx, int32_t cap, int32_t* iters_per_step,
+                       double* resid_per_step, int32_t* n_out);
+
+double yy_time(const yy_ctx* ctx);
+const char* yy_last_error(const yy_ctx* ctx);
+void yy_destroy(yy_ctx* ctx);   /* NULL is a no-op */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* YY_H */
