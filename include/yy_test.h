@@ -1,0 +1,34 @@
+/*
+ * yy_test.h — test and kernel-only entry points of the Yin-Yang step library.
+ * Not part of the user API; used by tests/ (unit parity of internal stages)
+ * and by bench.py's C4 kernel-only workload.
+ */
+#ifndef YY_TEST_H
+#define YY_TEST_H
+#include "yy.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Copy an internal per-step array of one patch to the host.  Names:
+ * "astar_r" | "astar_t" | "astar_p"  (a* = u2^{*,n+1/2}) and
+ * "G_T" | "G_ur1" | "G_ut1" | "G_up1" | "G_ur2" | "G_ut2" | "G_up2"
+ * (static right-hand sides G_q of the LAST step taken).
+ * host must hold the kind's full staggered array. */
+yy_status yy_debug_get(yy_ctx* ctx, const char* name, int32_t patch, double* host);
+
+/* C4 kernel-only operator: for ONE patch of ctx's grid solve
+ * (I - dt/2 A_axis) x = b on every line of `axis` (0 r, 1 theta, 2 phi) of the
+ * temperature operator (eq:Convect_Douglas factors, hat operators, transport
+ * velocity a* given by d_ar (nr+1,nt,np), d_at (nr,nt+1,np), d_ap (nr,nt,np+1)).
+ * d_x (nr,nt,np) holds b on entry and x on exit at the solved nodes (fringe
+ * layer untouched; homogeneous end conditions, wall ghost rule RD23).
+ * All pointers are DEVICE pointers; asynchronous on ctx's stream. */
+yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar, const double* d_at,
+                        const double* d_ap, double* d_x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,676 @@
+// yy_api.cu — the C ABI of include/yy.h: context, host-side geometry tables,
+// Yin<->Yang stencil construction, and the per-step launch sequence
+// (SURVEY.md §3 (ii)).  Device work is entirely in yy_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/yy.h"
+#include "../../include/yy_test.h"
+#include "yy_dev.cuh"
+#include "yy_internal.h"
+
+using namespace yy;
+
+namespace {
+
+// field slots (both patches contiguous per array)
+enum { FT = 0, FP1, FP2, FUR1, FUT1, FUP1, FUR2, FUT2, FUP2, NF };
+constexpr int FKIND[NF] = {KC, KC, KC, KR, KT, KP, KR, KT, KP};
+// wall fields
+enum { WT = 0, WUR, WUT, WUP, NW };
+constexpr int WKIND[NW] = {KC, KR, KT, KP};
+
+double tf_value(int tf, double t) {
+  switch (tf) {
+    case YY_TF_ONE: return 1.0;
+    case YY_TF_COS: return std::cos(t);
+    case YY_TF_SIN: return std::sin(t);
+    case YY_TF_COS2: return std::cos(t) * std::cos(t);
+  }
+  return 0.0;
+}
+
+}  // namespace
+
+struct yy_ctx {
+  Geo g{};
+  double R1 = 1, R2 = 2, Pr = 1, Ra = 0, dt = 1e-3, chi = 1.0;
+  int max_iters = 100, fixed_iters = 0;
+  double t = 0.0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  bool dead = false;
+  double* tab1d = nullptr;
+  double* n[NF] = {};
+  double* m[NF] = {};
+  double* it[NF] = {};
+  double* astar[3] = {};
+  double* G[NF] = {};
+  double* R = nullptr;
+  double* C = nullptr;
+  double* part = nullptr;
+  int maxb = 0;
+  double* red = nullptr;
+  double* red_host = nullptr;   // pinned
+  double* wterm[2][MAXSRC][NW] = {};
+  int nw[2] = {0, 0};
+  int wtf[2][MAXSRC] = {};
+  double* wl[3][NW] = {};       // wall data at t_{n-1}, t_n, t_{n+1}
+  double* sterm[2][MAXSRC][4] = {};
+  int ns[2] = {0, 0};
+  int stf[2][MAXSRC] = {};
+  // interpolation tables (device)
+  std::vector<void*> allocs;
+  CCTab tcc{};
+  VecTab tth{}, tph{};
+  std::vector<int> st_iters;
+  std::vector<double> st_rho;
+};
+
+namespace {
+
+yy_status fail(yy_ctx* c, yy_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  if (c && s == YY_ECUDA) c->dead = true;
+  return s;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, YY_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+yy_status dalloc(yy_ctx* ctx, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+  if (e != cudaSuccess) return fail(ctx, YY_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  ctx->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return YY_OK;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    yy_status s_ = (x);             \
+    if (s_ != YY_OK) return s_;     \
+  } while (0)
+
+// ---- geometry (reading RD1/RD2; §2) --------------------------------------
+struct HostGeo {
+  int nr, nt, np;
+  double dr, dth, dph, th0, ph0, R1;
+};
+
+HostGeo host_geo(const yy_grid* gr, double R1, double R2) {
+  HostGeo h;
+  h.nr = gr->nr;
+  h.nt = gr->ntheta;
+  h.np = gr->nphi;
+  h.dr = (R2 - R1) / h.nr;
+  h.dth = M_PI / (2.0 * (h.nt - 4));
+  const double delta = 2.0 * h.dth;
+  h.dph = (1.5 * M_PI + 2.0 * delta) / h.np;
+  h.th0 = M_PI / 4 - delta;
+  h.ph0 = -0.75 * M_PI - delta;
+  h.R1 = R1;
+  return h;
+}
+
+// Yin (th, ph) -> the other chart's (th~, ph~); the map is an involution
+// (PAPER.md L143-144), so the same function serves Yang -> Yin.
+void map_other(double th, double ph, double* tt, double* pp) {
+  const double x = std::sin(th) * std::cos(ph), y = std::sin(th) * std::sin(ph), z = std::cos(th);
+  *tt = std::acos(std::fmax(-1.0, std::fmin(1.0, y)));
+  *pp = std::atan2(z, -x);
+}
+
+// M_ab = e_a(target chart) . e_b(donor chart) for a,b in (theta, phi) (RD5)
+void rot(double th, double ph, double M[2][2]) {
+  double tt, pp;
+  map_other(th, ph, &tt, &pp);
+  const double et[3] = {std::cos(th) * std::cos(ph), std::cos(th) * std::sin(ph), -std::sin(th)};
+  const double ep[3] = {-std::sin(ph), std::cos(ph), 0.0};
+  const double dt_[3] = {-std::cos(tt) * std::cos(pp), -std::sin(tt), std::cos(tt) * std::sin(pp)};
+  const double dp_[3] = {std::sin(pp), 0.0, std::cos(pp)};
+  auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
+  M[0][0] = dot(et, dt_);
+  M[0][1] = dot(et, dp_);
+  M[1][0] = dot(ep, dt_);
+  M[1][1] = dot(ep, dp_);
+}
+
+// 4-point Lagrange on a uniform lattice x_m = x0 + m h; base = ceil(s) - 2 (RD42)
+void lagr(double x, double x0, double h, int* base, double w[4]) {
+  const double s = (x - x0) / h;
+  const int b = (int)std::ceil(s) - 2;
+  const double u = s - b;
+  for (int a = 0; a < 4; ++a) {
+    double v = 1.0;
+    for (int q = 0; q < 4; ++q)
+      if (q != a) v *= (u - q) / (double)(a - q);
+    w[a] = v;
+  }
+  *base = b;
+}
+
+struct Lattice {   // (theta, phi) lattice of a kind
+  double t0, p0;
+  int nt, np;      // node counts
+};
+
+Lattice lattice(const HostGeo& h, int K) {
+  Lattice L;
+  L.t0 = (K == KT) ? h.th0 : h.th0 + 0.5 * h.dth;
+  L.p0 = (K == KP) ? h.ph0 : h.ph0 + 0.5 * h.dph;
+  L.nt = h.nt + (K == KT);
+  L.np = h.np + (K == KP);
+  return L;
+}
+
+bool stencil(const HostGeo& h, double th, double ph, int donorK, int* jb, int* kb, double* w8) {
+  double tt, pp;
+  map_other(th, ph, &tt, &pp);
+  Lattice L = lattice(h, donorK);
+  lagr(tt, L.t0, h.dth, jb, w8);
+  lagr(pp, L.p0, h.dph, kb, w8 + 4);
+  // donor stencil must use donor solved nodes only (never the donor fringe)
+  return *jb >= 1 && *jb + 3 <= L.nt - 2 && *kb >= 1 && *kb + 3 <= L.np - 2;
+}
+
+template <class T>
+yy_status upload(yy_ctx* ctx, const std::vector<T>& v, const T** out) {
+  T* d = nullptr;
+  TRY(dalloc(ctx, &d, v.size() ? v.size() : 1));
+  if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *out = d;
+  return YY_OK;
+}
+
+yy_status build_tables(yy_ctx* ctx, const HostGeo& h) {
+  // C / R fringe on the (theta_c, phi_c) lattice
+  {
+    Lattice L = lattice(h, KC);
+    std::vector<int> tj, tk, jb, kb;
+    std::vector<double> w;
+    for (int j = 0; j < L.nt; ++j)
+      for (int k = 0; k < L.np; ++k) {
+        if (!(j == 0 || j == L.nt - 1 || k == 0 || k == L.np - 1)) continue;
+        int b1, b2;
+        double w8[8];
+        if (!stencil(h, L.t0 + j * h.dth, L.p0 + k * h.dph, KC, &b1, &b2, w8))
+          return fail(ctx, YY_EINVAL, "overlap too small: fringe stencil reaches the donor fringe");
+        tj.push_back(j); tk.push_back(k); jb.push_back(b1); kb.push_back(b2);
+        w.insert(w.end(), w8, w8 + 8);
+      }
+    ctx->tcc.n = (int)tj.size();
+    TRY(upload(ctx, tj, &ctx->tcc.tj)); TRY(upload(ctx, tk, &ctx->tcc.tk));
+    TRY(upload(ctx, jb, &ctx->tcc.jb)); TRY(upload(ctx, kb, &ctx->tcc.kb));
+    TRY(upload(ctx, w, &ctx->tcc.w));
+  }
+  for (int which = 0; which < 2; ++which) {
+    const int K = which == 0 ? KT : KP;
+    VecTab& T = which == 0 ? ctx->tth : ctx->tph;
+    Lattice L = lattice(h, K);
+    std::vector<int> tj, tk, jbt, kbt, jbp, kbp;
+    std::vector<double> wt, wp, m0, m1;
+    for (int j = 0; j < L.nt; ++j)
+      for (int k = 0; k < L.np; ++k) {
+        if (!(j == 0 || j == L.nt - 1 || k == 0 || k == L.np - 1)) continue;
+        const double th = L.t0 + j * h.dth, ph = L.p0 + k * h.dph;
+        int b1, b2, b3, b4;
+        double w1[8], w2[8], M[2][2];
+        if (!stencil(h, th, ph, KT, &b1, &b2, w1) || !stencil(h, th, ph, KP, &b3, &b4, w2))
+          return fail(ctx, YY_EINVAL, "overlap too small: fringe stencil reaches the donor fringe");
+        rot(th, ph, M);
+        tj.push_back(j); tk.push_back(k);
+        jbt.push_back(b1); kbt.push_back(b2); jbp.push_back(b3); kbp.push_back(b4);
+        wt.insert(wt.end(), w1, w1 + 8);
+        wp.insert(wp.end(), w2, w2 + 8);
+        m0.push_back(M[which][0]);
+        m1.push_back(M[which][1]);
+      }
+    T.n = (int)tj.size();
+    TRY(upload(ctx, tj, &T.tj)); TRY(upload(ctx, tk, &T.tk));
+    TRY(upload(ctx, jbt, &T.jb_t)); TRY(upload(ctx, kbt, &T.kb_t));
+    TRY(upload(ctx, jbp, &T.jb_p)); TRY(upload(ctx, kbp, &T.kb_p));
+    TRY(upload(ctx, wt, &T.w_t)); TRY(upload(ctx, wp, &T.w_p));
+    TRY(upload(ctx, m0, &T.m0)); TRY(upload(ctx, m1, &T.m1));
+  }
+  return YY_OK;
+}
+
+long long fsize(const yy_ctx* ctx, int f) { return psize(ctx->g, FKIND[f]); }
+
+yy_status check_args(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system) {
+  if (!ctx) return YY_EINVAL;
+  if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  if (patch < 0 || patch > 1) return fail(ctx, YY_EINVAL, "patch must be 0 (Yin) or 1 (Yang)");
+  if (level < 0 || level > 1) return fail(ctx, YY_EINVAL, "level must be 0 (t^n) or 1 (t^{n-1})");
+  if (system < 0 || system > 2) return fail(ctx, YY_EINVAL, "system must be 0, 1 or 2");
+  return YY_OK;
+}
+
+// ---- one time step ------------------------------------------------
+yy_status eval_walls(yy_ctx* ctx, int L, double t) {
+  const Geo& g = ctx->g;
+  for (int f = 0; f < NW; ++f) {
+    const long long ws = 2 * wsize(g, WKIND[f]);
+    for (int p = 0; p < 2; ++p) {
+      LinIn in{};
+      int nin = 0;
+      for (int m = 0; m < ctx->nw[p]; ++m)
+        if (ctx->wterm[p][m][f]) {
+          in.p[nin] = ctx->wterm[p][m][f];
+          in.c[nin] = tf_value(ctx->wtf[p][m], t);
+          ++nin;
+        }
+      launch_lincomb(ctx->wl[L][f] + p * ws, ws, in, nin, ctx->st);
+    }
+  }
+  return YY_OK;
+}
+
+StaticArgs static_args(yy_ctx* ctx, int q, double tsrc) {
+  StaticArgs a{};
+  a.ar = ctx->astar[0]; a.at = ctx->astar[1]; a.ap = ctx->astar[2];
+  const int f1 = (q == QT) ? FT : (q == QUR ? FUR1 : q == QUT ? FUT1 : FUP1);
+  const int f2 = (q == QT) ? FT : f1 + 3;
+  a.fn[0] = ctx->n[f1]; a.fn[1] = ctx->n[f2];
+  a.fm[0] = ctx->m[f1]; a.fm[1] = ctx->m[f2];
+  const int wf = (q == QT) ? WT : (q == QUR ? -1 : q == QUT ? WUT : WUP);
+  a.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
+  a.wm = wf >= 0 ? ctx->wl[0][wf] : nullptr;
+  a.p[0] = ctx->n[FP1]; a.p[1] = ctx->n[FP2];
+  a.utn[0] = ctx->n[FUT1]; a.utn[1] = ctx->n[FUT2];
+  a.utm[0] = ctx->m[FUT1]; a.utm[1] = ctx->m[FUT2];
+  a.upn[0] = ctx->n[FUP1]; a.upn[1] = ctx->n[FUP2];
+  a.upm[0] = ctx->m[FUP1]; a.upm[1] = ctx->m[FUP2];
+  const int sf = (q == QT) ? 0 : q;    // source field index: T, ur, ut, up
+  for (int p = 0; p < 2; ++p) {
+    int k = 0;
+    for (int m = 0; m < ctx->ns[p]; ++m)
+      if (ctx->sterm[p][m][sf]) {
+        a.src[p][k] = ctx->sterm[p][m][sf];
+        a.gsrc[p][k] = tf_value(ctx->stf[p][m], tsrc);
+        ++k;
+      }
+    a.nsrc[p] = k;
+  }
+  a.G[0] = ctx->G[f1];
+  a.G[1] = ctx->G[f2];
+  return a;
+}
+
+// factor orders as printed (RD28): first factor solved first
+constexpr int ORDER[4][3] = {{0, 1, 2}, {1, 2, 0}, {2, 0, 1}, {0, 1, 2}};
+
+yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
+  const Geo& g = ctx->g;
+  const int f = (q == QT) ? FT : (q == QUR ? FUR1 : q == QUT ? FUT1 : FUP1) + (s == 2 ? 3 : 0);
+  ResidArgs r{};
+  r.it = ctx->it[f];
+  r.n = ctx->n[f];
+  const int wf = (q == QT) ? WT : (q == QUR ? -1 : q == QUT ? WUT : WUP);
+  r.wnew = wf >= 0 ? ctx->wl[2][wf] : nullptr;
+  r.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
+  r.ar = ctx->astar[0]; r.at = ctx->astar[1]; r.ap = ctx->astar[2];
+  r.G = ctx->G[f];
+  r.R = ctx->R;
+  r.Tit = ctx->it[FT]; r.Tn = ctx->n[FT];
+  const int o = (s == 2) ? 3 : 0;
+  r.urit = ctx->it[FUR1 + o]; r.urn = ctx->n[FUR1 + o];
+  r.utit = ctx->it[FUT1 + o]; r.utn = ctx->n[FUT1 + o];
+  r.p1it = ctx->it[FP1]; r.p1n = ctx->n[FP1];
+  launch_resid(g, q, s, r, ctx->st);
+  SweepArgs w{};
+  w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
+  w.R = ctx->R; w.C = ctx->C; w.psi = ctx->it[f];
+  w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
+  w.maxb = ctx->maxb;
+  for (int a = 0; a < 3; ++a) {
+    const bool fin = (a == 2);
+    const int nb = launch_sweep(g, q, ORDER[q][a], fin, w, 2, ctx->st);
+    if (fin) nblk[slot] = nb;
+  }
+  return YY_OK;
+}
+
+yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
+  const Geo& g = ctx->g;
+  const double tau = ctx->dt, t = ctx->t;
+  cudaStream_t st = ctx->st;
+  // wall data at t_{n-1}, t_n, t_{n+1}
+  for (int L = 0; L < 3; ++L) TRY(eval_walls(ctx, L, t + (L - 1) * tau));
+  // O2: a* = 1.5 u2^n - 0.5 u2^{n-1}
+  for (int c = 0; c < 3; ++c) {
+    LinIn in{};
+    in.p[0] = ctx->n[FUR2 + c]; in.c[0] = 1.5;
+    in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
+    launch_lincomb(ctx->astar[c], 2 * fsize(ctx, FUR2 + c), in, 2, st);
+  }
+  // O3: static right-hand sides
+  for (int q = 0; q < 4; ++q) {
+    StaticArgs a = static_args(ctx, q, t + 0.5 * tau);
+    launch_static(g, q, a, st);
+  }
+  // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
+  for (int f = 0; f < NF; ++f)
+    CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], 2 * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const long long plane = (long long)g.nt * g.np;
+  for (int f : {FUR1, FUR2})
+    for (int p = 0; p < 2; ++p)
+      for (int w = 0; w < 2; ++w)
+        CK(cudaMemcpyAsync(ctx->it[f] + p * fsize(ctx, f) + (w ? g.nr * plane : 0),
+                           ctx->wl[2][WUR] + (p * 2 + w) * plane, plane * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+  InterpArgs ia{};
+  ia.cc[0] = ctx->it[FT]; ia.cc[1] = ctx->it[FP1]; ia.cc[2] = ctx->it[FP2];
+  ia.cc[3] = ctx->it[FUR1]; ia.cc[4] = ctx->it[FUR2];
+  ia.ut[0] = ctx->it[FUT1]; ia.ut[1] = ctx->it[FUT2];
+  ia.up[0] = ctx->it[FUP1]; ia.up[1] = ctx->it[FUP2];
+  ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
+  const int kmax = ctx->fixed_iters > 0 ? ctx->fixed_iters : ctx->max_iters;
+  int k = 0;
+  double rho = INFINITY;
+  ReduceArgs ra{};
+  ra.maxb = ctx->maxb;
+  while (k < kmax) {
+    ++k;
+    launch_interp(g, ia, st);                              // O5
+    TRY(solve_quantity(ctx, QT, 1, 0, ra.nblk));           // O6
+    for (int s = 1; s <= 2; ++s) {                         // O7 / O9
+      const int base = (s == 1) ? 1 : 5;
+      TRY(solve_quantity(ctx, QUR, s, base + 0, ra.nblk));
+      TRY(solve_quantity(ctx, QUT, s, base + 1, ra.nblk));
+      TRY(solve_quantity(ctx, QUP, s, base + 2, ra.nblk));
+      PresArgs pa{};
+      const int o = (s == 2) ? 3 : 0;
+      pa.urit = ctx->it[FUR1 + o]; pa.urn = ctx->n[FUR1 + o];
+      pa.utit = ctx->it[FUT1 + o]; pa.utn = ctx->n[FUT1 + o];
+      pa.upit = ctx->it[FUP1 + o]; pa.upn = ctx->n[FUP1 + o];
+      pa.pn = ctx->n[s == 1 ? FP1 : FP2];
+      pa.p1it = ctx->it[FP1]; pa.p1n = ctx->n[FP1];
+      pa.pit = ctx->it[s == 1 ? FP1 : FP2];
+      pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
+      pa.maxb = ctx->maxb;
+      ra.nblk[base + 3] = launch_pres(g, s, pa, st);
+    }
+    launch_reduce(ctx->part, ra, ctx->red, st);            // O10
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    rho = ctx->red_host[0];
+    if (ctx->red_host[1] != 0.0) return fail(ctx, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
+    if (ctx->fixed_iters <= 0 && rho < tol) break;
+  }
+  // O11: rotate levels
+  for (int f = 0; f < NF; ++f) {
+    if (f == FP1 || f == FP2) {
+      std::swap(ctx->n[f], ctx->it[f]);
+    } else {
+      double* tmp = ctx->m[f];
+      ctx->m[f] = ctx->n[f];
+      ctx->n[f] = ctx->it[f];
+      ctx->it[f] = tmp;
+    }
+  }
+  ctx->t = t + tau;
+  *iters = k;
+  *rho_out = rho;
+  return YY_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, yy_ctx** out) {
+  if (!out) return YY_EINVAL;
+  *out = nullptr;
+  if (!gr || gr->nr < 2 || gr->ntheta < 8 || gr->nphi < 8) return YY_EINVAL;
+  if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
+  yy_ctx* ctx = new yy_ctx();
+  ctx->R1 = R1; ctx->R2 = R2; ctx->Pr = Pr; ctx->Ra = Ra; ctx->dt = dt;
+  HostGeo h = host_geo(gr, R1, R2);
+  Geo& g = ctx->g;
+  g.nr = h.nr; g.nt = h.nt; g.np = h.np;
+  g.dr = h.dr; g.dth = h.dth; g.dph = h.dph; g.R1 = R1;
+  g.tau = dt; g.nu = Pr; g.kap = 1.0;
+  g.cchi = 1.0 / (2.0 * ctx->chi); g.inv_chi = 1.0 / ctx->chi; g.PrRa = Pr * Ra;
+  const double th1 = M_PI / 4 - 2.0 * h.dth;   // RD31
+  g.hatph = 1.0 / (R1 * R1 * std::sin(th1) * std::sin(th1) * h.dph * h.dph);
+  // 1-D tables
+  std::vector<double> tab;
+  for (int i = 0; i < h.nr; ++i) tab.push_back(R1 + (i + 0.5) * h.dr);
+  for (int i = 0; i <= h.nr; ++i) tab.push_back(R1 + i * h.dr);
+  for (int j = 0; j < h.nt; ++j) tab.push_back(std::sin(h.th0 + (j + 0.5) * h.dth));
+  for (int j = 0; j <= h.nt; ++j) tab.push_back(std::sin(h.th0 + j * h.dth));
+  for (int j = 0; j < h.nt; ++j) tab.push_back(std::cos(h.th0 + (j + 0.5) * h.dth));
+  for (int j = 0; j <= h.nt; ++j) tab.push_back(std::cos(h.th0 + j * h.dth));
+  yy_status s;
+  const double* dtab = nullptr;
+  if ((s = upload(ctx, tab, &dtab)) != YY_OK) { yy_destroy(ctx); return s; }
+  g.rc = dtab;
+  g.rf = g.rc + h.nr;
+  g.sc = g.rf + h.nr + 1;
+  g.sf = g.sc + h.nt;
+  g.cc = g.sf + h.nt + 1;
+  g.cf = g.cc + h.nt;
+  if ((s = build_tables(ctx, h)) != YY_OK) { std::fprintf(stderr, "yy_create: %s\n", ctx->err.c_str()); yy_destroy(ctx); return s; }
+  // fields
+  long long maxk = 0;
+  for (int K = 0; K < 4; ++K) maxk = std::max(maxk, psize(g, K));
+  for (int f = 0; f < NF; ++f) {
+    const size_t sz = 2 * psize(g, FKIND[f]);
+    if ((s = dalloc(ctx, &ctx->n[f], sz)) != YY_OK || (s = dalloc(ctx, &ctx->it[f], sz)) != YY_OK) { yy_destroy(ctx); return s; }
+    if (f != FP1 && f != FP2) {
+      if ((s = dalloc(ctx, &ctx->m[f], sz)) != YY_OK || (s = dalloc(ctx, &ctx->G[f], sz)) != YY_OK) { yy_destroy(ctx); return s; }
+    }
+    cudaMemset(ctx->n[f], 0, sz * sizeof(double));
+    cudaMemset(ctx->it[f], 0, sz * sizeof(double));
+    if (ctx->m[f]) cudaMemset(ctx->m[f], 0, sz * sizeof(double));
+    if (ctx->G[f]) cudaMemset(ctx->G[f], 0, sz * sizeof(double));
+  }
+  for (int c = 0; c < 3; ++c)
+    if ((s = dalloc(ctx, &ctx->astar[c], 2 * psize(g, KR + c))) != YY_OK) { yy_destroy(ctx); return s; }
+  if ((s = dalloc(ctx, &ctx->R, 2 * maxk)) != YY_OK || (s = dalloc(ctx, &ctx->C, 2 * maxk)) != YY_OK) { yy_destroy(ctx); return s; }
+  cudaMemset(ctx->R, 0, 2 * maxk * sizeof(double));
+  // norm partials: max blocks per (slot, patch)
+  long long mb = 0;
+  for (int K = 0; K < 4; ++K) {
+    mb = std::max(mb, (long long)((NPk(g, K) + 127) / 128) * NTk(g, K) * NRk(g, K));
+    mb = std::max(mb, (long long)((NTk(g, K) + 127) / 128) * NRk(g, K));
+  }
+  ctx->maxb = (int)mb;
+  if ((s = dalloc(ctx, &ctx->part, (size_t)NSLOT * 2 * mb)) != YY_OK || (s = dalloc(ctx, &ctx->red, 2 + 2 * NSLOT)) != YY_OK) { yy_destroy(ctx); return s; }
+  cudaMemset(ctx->part, 0, (size_t)NSLOT * 2 * mb * sizeof(double));
+  if (cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) { yy_destroy(ctx); return YY_ENOMEM; }
+  for (int L = 0; L < 3; ++L)
+    for (int f = 0; f < NW; ++f)
+      if ((s = dalloc(ctx, &ctx->wl[L][f], 4 * wsize(g, WKIND[f]))) != YY_OK) { yy_destroy(ctx); return s; }
+  if (cudaDeviceSynchronize() != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
+  *out = ctx;
+  return YY_OK;
+}
+
+yy_status yy_set_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system, const yy_fields* f) {
+  TRY(check_args(ctx, patch, level, system));
+  if (!f) return fail(ctx, YY_EINVAL, "NULL fields");
+  const int sys_lo = system == 0 ? 1 : system, sys_hi = system == 0 ? 2 : system;
+  double** L = level == 0 ? ctx->n : ctx->m;
+  auto put = [&](int fidx, const double* src) -> yy_status {
+    if (!src) return YY_OK;
+    const long long sz = fsize(ctx, fidx);
+    CK(cudaMemcpy(L[fidx] + patch * sz, src, sz * sizeof(double), cudaMemcpyHostToDevice));
+    return YY_OK;
+  };
+  for (int s = sys_lo; s <= sys_hi; ++s) {
+    const int o = (s == 2) ? 3 : 0;
+    TRY(put(FUR1 + o, f->ur));
+    TRY(put(FUT1 + o, f->ut));
+    TRY(put(FUP1 + o, f->up));
+    if (level == 0) TRY(put(s == 1 ? FP1 : FP2, f->p));
+  }
+  TRY(put(FT, f->T));
+  return YY_OK;
+}
+
+yy_status yy_get_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system, yy_fields* f) {
+  TRY(check_args(ctx, patch, level, system));
+  if (!f || system == 0) return fail(ctx, YY_EINVAL, "get_fields needs system 1 or 2");
+  double** L = level == 0 ? ctx->n : ctx->m;
+  auto get = [&](int fidx, double* dst) -> yy_status {
+    if (!dst) return YY_OK;
+    const long long sz = fsize(ctx, fidx);
+    CK(cudaMemcpy(dst, L[fidx] + patch * sz, sz * sizeof(double), cudaMemcpyDeviceToHost));
+    return YY_OK;
+  };
+  const int o = (system == 2) ? 3 : 0;
+  TRY(get(FUR1 + o, f->ur));
+  TRY(get(FUT1 + o, f->ut));
+  TRY(get(FUP1 + o, f->up));
+  if (level == 0) TRY(get(system == 1 ? FP1 : FP2, f->p));
+  TRY(get(FT, f->T));
+  return YY_OK;
+}
+
+static yy_status set_terms(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t* timefn,
+                           const yy_fields* terms, bool wall) {
+  if (!ctx) return YY_EINVAL;
+  if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  if (patch < 0 || patch > 1 || nterms < 0 || nterms > MAXSRC || (nterms > 0 && (!timefn || !terms)))
+    return fail(ctx, YY_EINVAL, "bad wall/source terms");
+  const Geo& g = ctx->g;
+  for (int m = 0; m < nterms; ++m)
+    if (timefn[m] < YY_TF_ONE || timefn[m] > YY_TF_COS2) return fail(ctx, YY_EINVAL, "bad time function");
+  for (int m = 0; m < nterms; ++m) {
+    const double* src[4] = {terms[m].T, terms[m].ur, terms[m].ut, terms[m].up};
+    for (int f = 0; f < 4; ++f) {
+      double*& slot = wall ? ctx->wterm[patch][m][f] : ctx->sterm[patch][m][f];
+      if (!src[f]) { slot = nullptr; continue; }
+      const long long sz = wall ? 2 * wsize(g, WKIND[f]) : psize(g, WKIND[f]);
+      double* d = nullptr;
+      TRY(dalloc(ctx, &d, sz));
+      CK(cudaMemcpy(d, src[f], sz * sizeof(double), cudaMemcpyHostToDevice));
+      slot = d;
+    }
+    (wall ? ctx->wtf : ctx->stf)[patch][m] = timefn[m];
+  }
+  (wall ? ctx->nw : ctx->ns)[patch] = nterms;
+  return YY_OK;
+}
+
+yy_status yy_set_wall(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t* timefn, const yy_fields* terms) {
+  return set_terms(ctx, patch, nterms, timefn, terms, true);
+}
+
+yy_status yy_set_source(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t* timefn, const yy_fields* terms) {
+  return set_terms(ctx, patch, nterms, timefn, terms, false);
+}
+
+yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
+  if (!ctx) return YY_EINVAL;
+  switch (key) {
+    case YY_CHI:
+      if (!(v > 0)) return fail(ctx, YY_EINVAL, "chi must be > 0");
+      ctx->chi = v;
+      ctx->g.cchi = 1.0 / (2.0 * v);
+      ctx->g.inv_chi = 1.0 / v;
+      return YY_OK;
+    case YY_MAX_ITERS:
+      if (v < 1) return fail(ctx, YY_EINVAL, "max_iters must be >= 1");
+      ctx->max_iters = (int)v;
+      return YY_OK;
+    case YY_FIXED_ITERS:
+      if (v < 0) return fail(ctx, YY_EINVAL, "fixed_iters must be >= 0");
+      ctx->fixed_iters = (int)v;
+      return YY_OK;
+  }
+  return fail(ctx, YY_EINVAL, "unknown parameter key");
+}
+
+yy_status yy_set_stream(yy_ctx* ctx, void* stream) {
+  if (!ctx) return YY_EINVAL;
+  ctx->st = static_cast<cudaStream_t>(stream);
+  return YY_OK;
+}
+
+yy_status yy_step(yy_ctx* ctx, int32_t nsteps, double tol) {
+  if (!ctx) return YY_EINVAL;
+  if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  if (nsteps < 0 || !(tol > 0)) return fail(ctx, YY_EINVAL, "nsteps >= 0 and tol > 0 required");
+  yy_status res = YY_OK;
+  for (int s = 0; s < nsteps; ++s) {
+    int it = 0;
+    double rho = 0;
+    TRY(one_step(ctx, tol, &it, &rho));
+    ctx->st_iters.push_back(it);
+    ctx->st_rho.push_back(rho);
+    if (ctx->fixed_iters <= 0 && !(rho < tol)) res = YY_ENOCONV;
+  }
+  return res;
+}
+
+yy_status yy_get_stats(const yy_ctx* ctx, int32_t cap, int32_t* iters, double* resid, int32_t* n_out) {
+  if (!ctx || cap < 0) return YY_EINVAL;
+  const int n = (int)ctx->st_iters.size();
+  const int cnt = n < cap ? n : cap;
+  for (int q = 0; q < cnt; ++q) {
+    if (iters) iters[q] = ctx->st_iters[n - cnt + q];
+    if (resid) resid[q] = ctx->st_rho[n - cnt + q];
+  }
+  if (n_out) *n_out = cnt;
+  return YY_OK;
+}
+
+double yy_time(const yy_ctx* ctx) { return ctx ? ctx->t : 0.0; }
+
+const char* yy_last_error(const yy_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+void yy_destroy(yy_ctx* ctx) {
+  if (!ctx) return;
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->red_host) cudaFreeHost(ctx->red_host);
+  delete ctx;
+}
+
+// ---- test / kernel-only entry points (include/yy_test.h) ---------------------------
+yy_status yy_debug_get(yy_ctx* ctx, const char* name, int32_t patch, double* host) {
+  if (!ctx || !name || !host || patch < 0 || patch > 1) return YY_EINVAL;
+  const Geo& g = ctx->g;
+  const double* src = nullptr;
+  long long sz = 0;
+  static const char* gnames[NF] = {"G_T", "", "", "G_ur1", "G_ut1", "G_up1", "G_ur2", "G_ut2", "G_up2"};
+  for (int f = 0; f < NF; ++f)
+    if (gnames[f][0] && !std::strcmp(name, gnames[f])) { src = ctx->G[f]; sz = psize(g, FKIND[f]); }
+  static const char* anames[3] = {"astar_r", "astar_t", "astar_p"};
+  for (int c = 0; c < 3; ++c)
+    if (!std::strcmp(name, anames[c])) { src = ctx->astar[c]; sz = psize(g, KR + c); }
+  if (!src) return fail(ctx, YY_EINVAL, std::string("unknown debug array ") + name);
+  CK(cudaMemcpy(host, src + patch * sz, sz * sizeof(double), cudaMemcpyDeviceToHost));
+  return YY_OK;
+}
+
+}  // extern "C"
+
+extern "C" yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar, const double* d_at,
+                                   const double* d_ap, double* d_x) {
+  if (!ctx || axis < 0 || axis > 2 || !d_ar || !d_at || !d_ap || !d_x) return YY_EINVAL;
+  if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  SweepArgs w{};
+  w.ar = d_ar; w.at = d_at; w.ap = d_ap;
+  w.R = d_x; w.C = ctx->C; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
+  launch_sweep(ctx->g, QT, axis, false, w, 1, ctx->st);
+  CK(cudaGetLastError());
+  return YY_OK;
+}

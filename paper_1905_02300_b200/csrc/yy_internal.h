@@ -1,0 +1,102 @@
+// yy_internal.h — kernel argument blocks shared by yy_kernels.cu and yy_api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace yy {
+
+struct Geo;
+
+constexpr int NSLOT = 9;     // T, u1r, u1t, u1p, p1, u2r, u2t, u2p, p2 (convergence slots)
+constexpr int MAXSRC = 4;    // time-basis terms per patch
+
+struct LinIn {               // out = sum_m c[m] * p[m]
+  const double* p[8];
+  double c[8];
+};
+
+struct StaticArgs {
+  const double* fn[2];       // psi^n   (system 1, 2; T uses [0])
+  const double* fm[2];       // psi^{n-1}
+  const double* wn;          // wall data at t_n (2 patches x 2 walls x plane), NULL for u_r
+  const double* wm;          // wall data at t_{n-1}
+  const double *ar, *at, *ap;  // a*
+  const double* p[2];        // p1^n, p2^n
+  const double* utn[2];      // u_th^n, u_th^{n-1} per system (for u_th^*)
+  const double* utm[2];
+  const double* upn[2];
+  const double* upm[2];
+  const double* src[2][MAXSRC];   // [patch][term] source arrays of this quantity
+  double gsrc[2][MAXSRC];
+  int nsrc[2];
+  double* G[2];
+};
+
+struct ResidArgs {
+  const double* it;          // psi~ (iterate with fresh fringe / walls)
+  const double* n;           // psi^n
+  const double* wnew;        // wall data t_{n+1}
+  const double* wn;          // wall data t_n
+  const double *ar, *at, *ap;
+  const double* G;
+  double* R;
+  const double *Tit, *Tn;    // for u_r buoyancy
+  const double *urit, *urn;  // this system's u_r (iterate, level n)
+  const double *utit, *utn;
+  const double *p1it, *p1n;
+};
+
+struct SweepArgs {
+  const double *ar, *at, *ap;
+  double* R;                 // in: rhs, out: solution (non-final)
+  double* C;                 // c' scratch
+  double* psi;               // FINAL: psi += x
+  double* part;              // FINAL: norm partials of this slot (2 * maxb)
+  int maxb;
+};
+
+struct PresArgs {
+  const double *urit, *urn, *utit, *utn, *upit, *upn;
+  const double* pn;          // this system's p^n
+  const double *p1it, *p1n;  // system 2 only
+  double* pit;               // this system's p iterate (updated in place)
+  double* part;
+  int maxb;
+};
+
+struct ReduceArgs {
+  int nblk[NSLOT];
+  int maxb;
+};
+
+struct CCTab {               // fringe of kinds C / R on the (theta_c, phi_c) lattice
+  int n;
+  const int *tj, *tk, *jb, *kb;
+  const double* w;           // [n][8]: wt[4], wp[4]
+};
+
+struct VecTab {              // fringe of kind TH or PH
+  int n;
+  const int *tj, *tk;
+  const int *jb_t, *kb_t, *jb_p, *kb_p;
+  const double *w_t, *w_p;   // [n][8]
+  const double *m0, *m1;     // rotation row
+};
+
+struct InterpArgs {
+  double* cc[5];             // T, p1, p2, u1r, u2r iterates (both patches)
+  double* ut[2];
+  double* up[2];
+  CCTab tab_cc;
+  VecTab tab_th, tab_ph;
+};
+
+void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);
+void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st);
+void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t st);
+int launch_sweep(const Geo& g, int q, int ax, bool fin, const SweepArgs& a, int npatch, cudaStream_t st);
+int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st);
+void launch_reduce(const double* part, const ReduceArgs& a, double* out, cudaStream_t st);
+void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st);
+
+}  // namespace yy

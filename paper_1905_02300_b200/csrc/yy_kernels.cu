@@ -1,0 +1,563 @@
+// yy_kernels.cu — sm_100a fp64 kernels of one Yin-Yang AC direction-splitting
+// time step (arXiv 1905.02300).  Launch wrappers at the bottom are called by
+// yy_api.cu.  Every step of the hot path runs here; the host only sequences
+// launches.
+//
+// Kernels (SURVEY.md §2.2 naming):
+//   K0  k_static<Q>      per-step static RHS G_q (O3), both systems fused
+//   K1  k_resid<Q,S>     eq:er residual R = G + tau E_dyn - (I - tau/2 L_split)(psi~ - psi^n)
+//   K2/K3 k_sweep<Q,AX,F> batched Thomas along AX, rows from coef<> (one line per thread)
+//   K5  k_interp_*       Yin<->Yang fringe interpolation (4x4 Lagrange, rotation)
+//   K6  k_reduce         deterministic Schwarz residual reduction
+//   K7  k_pres<S>        pressure updates eq:nst_Mass1 / eq:ac2 (RD18)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "yy_dev.cuh"
+#include "yy_internal.h"
+
+namespace yy {
+
+// ---------------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------------
+struct Star {   // 7-point star of a field at a node; x = r, y = theta, z = phi
+  double c, xm, xp, ym, yp, zm, zp;
+};
+
+__device__ __forceinline__ Star star_lin(const Star& a, double fa, const Star& b, double fb) {
+  Star s;
+  s.c = fa * a.c + fb * b.c;
+  s.xm = fa * a.xm + fb * b.xm;
+  s.xp = fa * a.xp + fb * b.xp;
+  s.ym = fa * a.ym + fb * b.ym;
+  s.yp = fa * a.yp + fb * b.yp;
+  s.zm = fa * a.zm + fb * b.zm;
+  s.zp = fa * a.zp + fb * b.zp;
+  return s;
+}
+
+// Star of field F (one patch) at (i,j,k).  For r-centred kinds the r
+// neighbours beyond the walls are the ghosts 2 w - psi_0 (reading RD22),
+// W = the field's wall data (2, NT, NP) at the matching time level.
+template <int K>
+__device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict__ F,
+                                          const double* __restrict__ W, int i, int j, int k) {
+  Star s;
+  s.c = F[IX<K>(g, i, j, k)];
+  if (K != KR && i == 0) s.xm = 2.0 * W[(long long)j * NPk(g, K) + k] - s.c;
+  else s.xm = F[IX<K>(g, i - 1, j, k)];
+  if (K != KR && i == g.nr - 1) s.xp = 2.0 * W[wsize(g, K) + (long long)j * NPk(g, K) + k] - s.c;
+  else s.xp = F[IX<K>(g, i + 1, j, k)];
+  s.ym = F[IX<K>(g, i, j - 1, k)];
+  s.yp = F[IX<K>(g, i, j + 1, k)];
+  s.zm = F[IX<K>(g, i, j, k - 1)];
+  s.zp = F[IX<K>(g, i, j, k + 1)];
+  return s;
+}
+
+// sum_d L_{Q,d} applied to a star.
+template <int Q, bool HAT>
+__device__ __forceinline__ double applyL(const Geo& g, const Astar& A, int i, int j, int k, const Star& s) {
+  double am, a0, ap, acc;
+  coef<Q, 0, HAT>(g, A, i, j, k, am, a0, ap);
+  acc = am * s.xm + a0 * s.c + ap * s.xp;
+  coef<Q, 1, HAT>(g, A, i, j, k, am, a0, ap);
+  acc += am * s.ym + a0 * s.c + ap * s.yp;
+  coef<Q, 2, HAT>(g, A, i, j, k, am, a0, ap);
+  acc += am * s.zm + a0 * s.c + ap * s.zp;
+  return acc;
+}
+
+template <int K>
+__device__ __forceinline__ bool solved(const Geo& g, int i, int j, int k) {
+  return i >= i_lo<K>() && i <= i_hi<K>(g) && j >= 1 && j <= NTk(g, K) - 2 && k >= 1 && k <= NPk(g, K) - 2;
+}
+
+// divergence contributions at cell centre (i,j,k) of one patch
+__device__ __forceinline__ double div1(const Geo& g, const double* ur, int i, int j, int k) {
+  const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1), c = __ldg(g.rc + i);
+  return (f1 * f1 * ur[IX<KR>(g, i + 1, j, k)] - f0 * f0 * ur[IX<KR>(g, i, j, k)]) / (c * c * g.dr);
+}
+__device__ __forceinline__ double div2(const Geo& g, const double* ut, int i, int j, int k) {
+  return (__ldg(g.sf + j + 1) * ut[IX<KT>(g, i, j + 1, k)] - __ldg(g.sf + j) * ut[IX<KT>(g, i, j, k)]) /
+         (__ldg(g.rc + i) * __ldg(g.sc + j) * g.dth);
+}
+__device__ __forceinline__ double div3(const Geo& g, const double* up, int i, int j, int k) {
+  return (up[IX<KP>(g, i, j, k + 1)] - up[IX<KP>(g, i, j, k)]) / (__ldg(g.rc + i) * __ldg(g.sc + j) * g.dph);
+}
+
+__device__ __forceinline__ double omega(const Geo& g, double r, double s) {
+  return r * r * s * g.dr * g.dth * g.dph;
+}
+
+// deterministic block sum (fixed thread -> data assignment, fixed tree)
+template <int NT_>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[NT_ / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int q = 0; q < NT_ / 32; ++q) t += sh[q];
+  return t;   // valid in thread 0
+}
+
+// ---------------------------------------------------------------------------------
+// elementwise
+// ---------------------------------------------------------------------------------
+// out = sum_m c[m] * in[m]   (a* extrapolation O2, wall/time-basis evaluation)
+__global__ void k_lincomb(double* __restrict__ out, long long n, int nin, LinIn in) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (; idx < n; idx += stride) {
+    double v = 0.0;
+    for (int m = 0; m < nin; ++m) v += in.c[m] * in.p[m][idx];
+    out[idx] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K0: static right-hand side G (O3):  G = tau [L_full psi^* - 1/2 L_split (psi^n - psi^{n-1}) + E_static]
+// grid: x -> k, y -> j, z -> patch * NR + i
+// ---------------------------------------------------------------------------------
+template <int Q>
+__global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
+  constexpr int K = kind_of(Q);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int patch = blockIdx.z / NRk(g, K);
+  const int i = blockIdx.z % NRk(g, K);
+  if (k >= NPk(g, K) || !solved<K>(g, i, j, k)) return;
+  const long long po = patch * psize(g, K);
+  const long long pc = patch * psize(g, KC);
+  const long long node = IX<K>(g, i, j, k);
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+  const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
+  const double* Wm = a.wm ? a.wm + patch * 2 * wsize(g, K) : nullptr;
+  double src = 0.0;
+  for (int m = 0; m < a.nsrc[patch]; ++m) src += a.gsrc[patch][m] * a.src[patch][m][node];
+
+  const double rn = rnode<K>(g, i);
+  const int nsys = (Q == QT) ? 1 : 2;
+  for (int s = 0; s < nsys; ++s) {
+    Star n = load_star<K>(g, a.fn[s] + po, Wn, i, j, k);
+    Star m = load_star<K>(g, a.fm[s] + po, Wm, i, j, k);
+    Star S = star_lin(n, 1.5, m, -0.5);
+    Star D = star_lin(n, 1.0, m, -1.0);
+    double E = src;
+    if (Q != QT) {
+      const double* p = a.p[s] + pc;
+      const double* uts = nullptr;
+      if (Q == QUR) {
+        // -d_r p^n + c_chi d_r(div2 u_th^* + div3 u_ph^*) + (a_th^2 + a_ph^2)/r   (eq:r_comp, RD17)
+        const long long ot = patch * psize(g, KT), op = patch * psize(g, KP);
+        const double *utn = a.utn[s] + ot, *utm = a.utm[s] + ot, *upn = a.upn[s] + op, *upm = a.upm[s] + op;
+        auto dd = [&](int ii) {
+          const double d2 = 1.5 * div2(g, utn, ii, j, k) - 0.5 * div2(g, utm, ii, j, k);
+          const double d3 = 1.5 * div3(g, upn, ii, j, k) - 0.5 * div3(g, upm, ii, j, k);
+          return d2 + d3;
+        };
+        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i - 1, j, k)]) / g.dr;
+        E += g.cchi * (dd(i) - dd(i - 1)) / g.dr;
+        const double at_ = abar_t<KR>(g, A, i, j, k), ap_ = abar_p<KR>(g, A, i, j, k);
+        E += (at_ * at_ + ap_ * ap_) / rn;
+        (void)uts;
+      } else if (Q == QUT) {
+        // -(1/r) d_th p^n + c_chi (1/r) d_th(div3 u_ph^*) + a_ph^2 cot(th)/r   (eq:theta_comp, RD14)
+        const long long op = patch * psize(g, KP);
+        const double *upn = a.upn[s] + op, *upm = a.upm[s] + op;
+        const double d3 = 1.5 * div3(g, upn, i, j, k) - 0.5 * div3(g, upm, i, j, k);
+        const double d3m = 1.5 * div3(g, upn, i, j - 1, k) - 0.5 * div3(g, upm, i, j - 1, k);
+        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i, j - 1, k)]) / (rn * g.dth);
+        E += g.cchi * (d3 - d3m) / (rn * g.dth);
+        const double ap_ = abar_p<KT>(g, A, i, j, k);
+        E += ap_ * ap_ * __ldg(g.cf + j) / (__ldg(g.sf + j) * rn);
+      } else {
+        // -(1/(r sin th)) d_ph p^n   (eq:phi_comp)
+        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i, j, k - 1)]) / (rn * __ldg(g.sc + j) * g.dph);
+      }
+    }
+    const double Lf = applyL<Q, false>(g, A, i, j, k, S);
+    const double Ls = applyL<Q, true>(g, A, i, j, k, D);
+    a.G[s][po + node] = g.tau * (Lf - 0.5 * Ls + E);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K1: residual of eq:er (sign RD9) with the Gauss-Seidel dynamic terms
+// ---------------------------------------------------------------------------------
+template <int Q, int S>
+__global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
+  constexpr int K = kind_of(Q);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int patch = blockIdx.z / NRk(g, K);
+  const int i = blockIdx.z % NRk(g, K);
+  if (k >= NPk(g, K) || !solved<K>(g, i, j, k)) return;
+  const long long po = patch * psize(g, K);
+  const long long pc = patch * psize(g, KC);
+  const long long node = IX<K>(g, i, j, k);
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+  const double* Wnew = a.wnew ? a.wnew + patch * 2 * wsize(g, K) : nullptr;
+  const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
+  Star x1 = load_star<K>(g, a.it + po, Wnew, i, j, k);
+  Star x0 = load_star<K>(g, a.n + po, Wn, i, j, k);
+  Star X = star_lin(x1, 1.0, x0, -1.0);
+  const double rn = rnode<K>(g, i);
+  double E = 0.0;
+  if (Q == QUR) {
+    // buoyancy +Pr Ra T^{n+1/2,(k)} e_r (RD20, RD21)
+    const double* Ti = a.Tit + pc;
+    const double* Tn = a.Tn + pc;
+    const double tb0 = 0.5 * (Ti[IX<KC>(g, i - 1, j, k)] + Tn[IX<KC>(g, i - 1, j, k)]);
+    const double tb1 = 0.5 * (Ti[IX<KC>(g, i, j, k)] + Tn[IX<KC>(g, i, j, k)]);
+    E = g.PrRa * 0.5 * (tb0 + tb1);
+  } else if (Q == QUT) {
+    // c_chi D21 ub_r + nu((2/r^2) d_th ub_r + (2 cos/(r^3 sin)) d_r(r^2 ub_r))  (eq:theta_comp)
+    const long long orr = patch * psize(g, KR);
+    const double *uri = a.urit + orr, *urn = a.urn + orr;
+    auto ub = [&](int ii, int jj) {
+      const long long q = IX<KR>(g, ii, jj, k);
+      return 0.5 * (uri[q] + urn[q]);
+    };
+    auto d1 = [&](int jj) {
+      const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1), c = __ldg(g.rc + i);
+      return (f1 * f1 * ub(i + 1, jj) - f0 * f0 * ub(i, jj)) / (c * c * g.dr);
+    };
+    const double d1a = d1(j - 1), d1b = d1(j);
+    E = g.cchi * (d1b - d1a) / (rn * g.dth);
+    E += g.nu * (2.0 / (rn * rn)) * 0.5 * ((ub(i, j) - ub(i, j - 1)) + (ub(i + 1, j) - ub(i + 1, j - 1))) / g.dth;
+    E += g.nu * (2.0 * __ldg(g.cf + j) / (__ldg(g.sf + j) * rn)) * 0.5 * (d1a + d1b);
+  } else if (Q == QUP) {
+    // c_chi (D31 ub_r + D32 ub_th) + nu((2/(r^2 sin)) d_ph ub_r + (2cos/(r^2 sin^2)) d_ph ub_th)
+    const long long orr = patch * psize(g, KR), ot = patch * psize(g, KT);
+    const double *uri = a.urit + orr, *urn = a.urn + orr, *uti = a.utit + ot, *utn = a.utn + ot;
+    auto ubr = [&](int ii, int kk) {
+      const long long q = IX<KR>(g, ii, j, kk);
+      return 0.5 * (uri[q] + urn[q]);
+    };
+    auto ubt = [&](int jj, int kk) {
+      const long long q = IX<KT>(g, i, jj, kk);
+      return 0.5 * (uti[q] + utn[q]);
+    };
+    const double sn = __ldg(g.sc + j), cn = __ldg(g.cc + j);
+    const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1);
+    const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1);
+    auto e = [&](int kk) {
+      const double dd1 = (f1 * f1 * ubr(i + 1, kk) - f0 * f0 * ubr(i, kk)) / (rn * rn * g.dr);
+      const double dd2 = (s1 * ubt(j + 1, kk) - s0 * ubt(j, kk)) / (rn * sn * g.dth);
+      return dd1 + dd2;
+    };
+    E = g.cchi * (e(k) - e(k - 1)) / (rn * sn * g.dph);
+    E += g.nu * (2.0 / (rn * rn * sn)) * 0.5 * ((ubr(i, k) - ubr(i, k - 1)) + (ubr(i + 1, k) - ubr(i + 1, k - 1))) / g.dph;
+    E += g.nu * (2.0 * cn / (rn * rn * sn * sn)) * 0.5 * ((ubt(j, k) - ubt(j, k - 1)) + (ubt(j + 1, k) - ubt(j + 1, k - 1))) / g.dph;
+  }
+  if (S == 2 && Q != QT) {
+    // -1/2 grad(p1^(k) - p1^n)   (RD18)
+    const double *pi_ = a.p1it + pc, *pn = a.p1n + pc;
+    auto dp = [&](int ii, int jj, int kk) {
+      const long long q = IX<KC>(g, ii, jj, kk);
+      return pi_[q] - pn[q];
+    };
+    if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) / g.dr;
+    if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) / (rn * g.dth);
+    if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) / (rn * __ldg(g.sc + j) * g.dph);
+  }
+  const double LX = applyL<Q, true>(g, A, i, j, k, X);
+  a.R[po + node] = a.G[po + node] + g.tau * E - (X.c - 0.5 * g.tau * LX);
+}
+
+// ---------------------------------------------------------------------------------
+// K2/K3: Thomas along AX for every line (one line per thread).  Rows
+// (I - tau/2 A_{Q,AX}) from coef<Q,AX,true>; homogeneous Dirichlet increments at
+// fringe / u_r wall faces; antisymmetric wall ghost for r-centred kinds (RD23).
+// In place on R (d' then x); c' in scratch C.  FINAL: psi += x and norm partial.
+// Line grid: AX=0: x -> k, y -> j;  AX=1: x -> k, y -> i;  AX=2: x -> j, y -> i.  z -> patch.
+// ---------------------------------------------------------------------------------
+template <int Q, int AX, bool FINAL>
+__global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
+  constexpr int K = kind_of(Q);
+  const int patch = blockIdx.z;
+  int i = 0, j = 0, k = 0, n = 0;
+  long long stride = 0;
+  const int tx = blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid;
+  if (AX == 0) {
+    k = tx + 1; j = blockIdx.y + 1; i = i_lo<K>();
+    valid = k <= NPk(g, K) - 2;
+    n = i_hi<K>(g) - i_lo<K>() + 1;
+    stride = (long long)NTk(g, K) * NPk(g, K);
+  } else if (AX == 1) {
+    k = tx + 1; i = blockIdx.y + i_lo<K>(); j = 1;
+    valid = k <= NPk(g, K) - 2;
+    n = NTk(g, K) - 2;
+    stride = NPk(g, K);
+  } else {
+    j = tx + 1; i = blockIdx.y + i_lo<K>(); k = 1;
+    valid = j <= NTk(g, K) - 2;
+    n = NPk(g, K) - 2;
+    stride = 1;
+  }
+  double wsum = 0.0;
+  if (valid) {
+    const long long po = patch * psize(g, K);
+    Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+    double* __restrict__ R = a.R + po;
+    double* __restrict__ C = a.C + po;
+    const long long base = IX<K>(g, i, j, k);
+    const double th = 0.5 * g.tau;
+    double cprev = 0.0, dprev = 0.0;
+    for (int m = 0; m < n; ++m) {
+      const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j, kk = (AX == 2) ? k + m : k;
+      double am, a0, ap;
+      coef<Q, AX, true>(g, A, ii, jj, kk, am, a0, ap);
+      double di = 1.0 - th * a0;
+      if (AX == 0 && K != KR) {
+        if (m == 0) di = 1.0 - th * (a0 - am);
+        if (m == n - 1) di = 1.0 - th * (a0 - ap);
+      }
+      const double lo = (m == 0) ? 0.0 : -th * am;
+      const double up = -th * ap;
+      const double inv = 1.0 / (di - lo * cprev);
+      const long long q = base + m * stride;
+      const double cp = up * inv;
+      const double dp = (R[q] - lo * dprev) * inv;
+      C[q] = cp;
+      R[q] = dp;
+      cprev = cp;
+      dprev = dp;
+    }
+    double x = 0.0;
+    double* __restrict__ psi = FINAL ? a.psi + po : nullptr;
+    for (int m = n - 1; m >= 0; --m) {
+      const long long q = base + m * stride;
+      x = (m == n - 1) ? R[q] : R[q] - C[q] * x;
+      if (FINAL) {
+        psi[q] += x;
+        const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j;
+        wsum += omega(g, rnode<K>(g, ii), snode<K>(g, jj)) * x * x;
+      } else {
+        R[q] = x;
+      }
+    }
+  }
+  if (FINAL) {
+    const double t = block_sum<128>(wsum);
+    if (threadIdx.x == 0)
+      a.part[(long long)patch * a.maxb + blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K7: pressure updates (eq:nst_Mass1 P:L457; system 2 per RD18)
+// ---------------------------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int patch = blockIdx.z / g.nr;
+  const int i = blockIdx.z % g.nr;
+  double w = 0.0;
+  if (k < g.np && solved<KC>(g, i, j, k)) {
+    const long long pc = patch * psize(g, KC);
+    const long long orr = patch * psize(g, KR), ot = patch * psize(g, KT), op = patch * psize(g, KP);
+    const double *uri = a.urit + orr, *urn = a.urn + orr;
+    const double *uti = a.utit + ot, *utn = a.utn + ot;
+    const double *upi = a.upit + op, *upn = a.upn + op;
+    const double rn = __ldg(g.rc + i), sn = __ldg(g.sc + j);
+    const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1);
+    const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1);
+    const double ur0 = 0.5 * (uri[IX<KR>(g, i, j, k)] + urn[IX<KR>(g, i, j, k)]);
+    const double ur1 = 0.5 * (uri[IX<KR>(g, i + 1, j, k)] + urn[IX<KR>(g, i + 1, j, k)]);
+    const double ut0 = 0.5 * (uti[IX<KT>(g, i, j, k)] + utn[IX<KT>(g, i, j, k)]);
+    const double ut1 = 0.5 * (uti[IX<KT>(g, i, j + 1, k)] + utn[IX<KT>(g, i, j + 1, k)]);
+    const double up0 = 0.5 * (upi[IX<KP>(g, i, j, k)] + upn[IX<KP>(g, i, j, k)]);
+    const double up1 = 0.5 * (upi[IX<KP>(g, i, j, k + 1)] + upn[IX<KP>(g, i, j, k + 1)]);
+    const double dv = (f1 * f1 * ur1 - f0 * f0 * ur0) / (rn * rn * g.dr) +
+                      (s1 * ut1 - s0 * ut0) / (rn * sn * g.dth) + (up1 - up0) / (rn * sn * g.dph);
+    const long long q = pc + IX<KC>(g, i, j, k);
+    double nv;
+    if (S == 1) nv = a.pn[q] - g.inv_chi * dv;
+    else nv = a.pn[q] + (a.p1it[q] - a.p1n[q]) - g.inv_chi * dv;
+    const double d = nv - a.pit[q];
+    a.pit[q] = nv;
+    w = omega(g, rn, sn) * d * d;
+  }
+  const double t = block_sum<128>(w);
+  if (threadIdx.x == 0) {
+    const int b = (blockIdx.z % g.nr) * gridDim.y * gridDim.x + blockIdx.y * gridDim.x + blockIdx.x;
+    a.part[(long long)(blockIdx.z / g.nr) * a.maxb + b] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K6: deterministic final reduction: 18 (quantity, patch) sums in fixed order,
+// rho = max sqrt; NaN/Inf -> flag.
+// ---------------------------------------------------------------------------------
+__global__ void k_reduce(const double* __restrict__ part, ReduceArgs a, double* __restrict__ out) {
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;   // one warp per (slot, patch)
+  __shared__ double sums[2 * NSLOT];
+  if (w < 2 * NSLOT) {
+    const int slot = w / 2, patch = w % 2;
+    const double* p = part + ((long long)slot * 2 + patch) * a.maxb;
+    const int nb = a.nblk[slot];
+    double v = 0.0;
+    for (int b = l; b < nb; b += 32) v += p[b];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (l == 0) sums[w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rho = 0.0;
+    int bad = 0;
+    for (int q = 0; q < 2 * NSLOT; ++q) {
+      const double s = sums[q];
+      if (!(s == s) || s > 1e300) bad = 1;
+      out[2 + q] = sqrt(s);
+      rho = fmax(rho, sqrt(s));
+    }
+    out[0] = bad ? __longlong_as_double(0x7ff8000000000000LL) : rho;
+    out[1] = bad;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K5: Yin<->Yang fringe interpolation (Alg.1 steps 1,3,7; RD3-RD5).
+// Reads donor solved nodes, writes target fringe nodes: race-free in place.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double interp16(const Geo& g, int K, const double* __restrict__ X, int i, int jb,
+                                           int kb, const double* __restrict__ w) {
+  const int NT = NTk(g, K), NP = NPk(g, K);
+  const double* base = X + ((long long)i * NT + jb) * NP + kb;
+  double v = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double* row = base + (long long)a * NP;
+    const double s = w[4] * row[0] + w[5] * row[1] + w[6] * row[2] + w[7] * row[3];
+    v += w[a] * s;
+  }
+  return v;
+}
+
+// scalar-like quantities on the (theta_c, phi_c) lattice: T, p1, p2, u_r1, u_r2
+// grid: x -> entry, y -> i (0..nr), z -> patch*5 + quantity
+__global__ void k_interp_cc(Geo g, InterpArgs a) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int patch = blockIdx.z / 5, q = blockIdx.z % 5;
+  if (e >= a.tab_cc.n) return;
+  const int K = (q < 3) ? KC : KR;
+  if (K == KC && i >= g.nr) return;
+  if (K == KR && (i < 1 || i > g.nr - 1)) return;
+  const long long ps = psize(g, K);
+  double* X = a.cc[q];
+  const double* donor = X + (1 - patch) * ps;
+  double* tgt = X + patch * ps;
+  const int jb = a.tab_cc.jb[e], kb = a.tab_cc.kb[e];
+  const double v = interp16(g, K, donor, i, jb, kb, a.tab_cc.w + 8LL * e);
+  tgt[((long long)i * NTk(g, K) + a.tab_cc.tj[e]) * NPk(g, K) + a.tab_cc.tk[e]] = v;
+}
+
+// tangential vector components: target kind KT (u_th) or KP (u_ph) of both
+// systems; both donor components interpolated on their own lattices, rotated.
+// grid: x -> entry, y -> i, z -> patch*2 + system
+template <int KTGT>
+__global__ void k_interp_vec(Geo g, InterpArgs a) {
+  const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int patch = blockIdx.z / 2, s = blockIdx.z % 2;
+  if (e >= t.n) return;
+  const double* ut = a.ut[s];
+  const double* up = a.up[s];
+  const double* dut = ut + (1 - patch) * psize(g, KT);
+  const double* dup = up + (1 - patch) * psize(g, KP);
+  const double vt = interp16(g, KT, dut, i, t.jb_t[e], t.kb_t[e], t.w_t + 8LL * e);
+  const double vp = interp16(g, KP, dup, i, t.jb_p[e], t.kb_p[e], t.w_p + 8LL * e);
+  const double v = t.m0[e] * vt + t.m1[e] * vp;
+  double* tgt = (KTGT == KT ? a.ut[s] : a.up[s]) + patch * psize(g, KTGT);
+  tgt[((long long)i * NTk(g, KTGT) + t.tj[e]) * NPk(g, KTGT) + t.tk[e]] = v;
+}
+
+// ---------------------------------------------------------------------------------
+// C4 kernel-only operator: one patch, T rows (hats), all lines of one axis.
+// ---------------------------------------------------------------------------------
+
+// ---------------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------------
+static inline dim3 pgrid(const Geo& g, int K, int npatch) {
+  return dim3((NPk(g, K) + 127) / 128, NTk(g, K), NRk(g, K) * npatch);
+}
+
+void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_lincomb<<<blocks, 256, 0, st>>>(out, n, nin, in);
+}
+
+void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st) {
+  switch (q) {
+    case QT: k_static<QT><<<pgrid(g, KC, 2), 128, 0, st>>>(g, a); break;
+    case QUR: k_static<QUR><<<pgrid(g, KR, 2), 128, 0, st>>>(g, a); break;
+    case QUT: k_static<QUT><<<pgrid(g, KT, 2), 128, 0, st>>>(g, a); break;
+    case QUP: k_static<QUP><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); break;
+  }
+}
+
+void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t st) {
+  if (q == QT) k_resid<QT, 1><<<pgrid(g, KC, 2), 128, 0, st>>>(g, a);
+  else if (q == QUR) { if (s == 1) k_resid<QUR, 1><<<pgrid(g, KR, 2), 128, 0, st>>>(g, a); else k_resid<QUR, 2><<<pgrid(g, KR, 2), 128, 0, st>>>(g, a); }
+  else if (q == QUT) { if (s == 1) k_resid<QUT, 1><<<pgrid(g, KT, 2), 128, 0, st>>>(g, a); else k_resid<QUT, 2><<<pgrid(g, KT, 2), 128, 0, st>>>(g, a); }
+  else { if (s == 1) k_resid<QUP, 1><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); else k_resid<QUP, 2><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); }
+}
+
+template <int Q, int AX, bool F>
+static int sweep_one(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  dim3 grid;
+  if (AX == 0) grid = dim3((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, npatch);
+  else if (AX == 1) grid = dim3((NPk(g, K) - 2 + 127) / 128, (K == KR ? g.nr - 1 : g.nr), npatch);
+  else grid = dim3((NTk(g, K) - 2 + 127) / 128, (K == KR ? g.nr - 1 : g.nr), npatch);
+  k_sweep<Q, AX, F><<<grid, 128, 0, st>>>(g, a);
+  return (int)(grid.x * grid.y);
+}
+
+template <int Q>
+static int sweep_axis(const Geo& g, int ax, bool fin, const SweepArgs& a, int npatch, cudaStream_t st) {
+  if (ax == 0) return fin ? sweep_one<Q, 0, true>(g, a, npatch, st) : sweep_one<Q, 0, false>(g, a, npatch, st);
+  if (ax == 1) return fin ? sweep_one<Q, 1, true>(g, a, npatch, st) : sweep_one<Q, 1, false>(g, a, npatch, st);
+  return fin ? sweep_one<Q, 2, true>(g, a, npatch, st) : sweep_one<Q, 2, false>(g, a, npatch, st);
+}
+
+int launch_sweep(const Geo& g, int q, int ax, bool fin, const SweepArgs& a, int npatch, cudaStream_t st) {
+  switch (q) {
+    case QT: return sweep_axis<QT>(g, ax, fin, a, npatch, st);
+    case QUR: return sweep_axis<QUR>(g, ax, fin, a, npatch, st);
+    case QUT: return sweep_axis<QUT>(g, ax, fin, a, npatch, st);
+    default: return sweep_axis<QUP>(g, ax, fin, a, npatch, st);
+  }
+}
+
+int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st) {
+  dim3 grid = pgrid(g, KC, 2);
+  if (s == 1) k_pres<1><<<grid, 128, 0, st>>>(g, a);
+  else k_pres<2><<<grid, 128, 0, st>>>(g, a);
+  return (int)(grid.x * grid.y * g.nr);
+}
+
+void launch_reduce(const double* part, const ReduceArgs& a, double* out, cudaStream_t st) {
+  k_reduce<<<1, 32 * 2 * NSLOT, 0, st>>>(part, a, out);
+}
+
+void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st) {
+  if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 10), 128, 0, st>>>(g, a);
+  if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, g.nr, 4), 128, 0, st>>>(g, a);
+  if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 4), 128, 0, st>>>(g, a);
+}
+
+}  // namespace yy

@@ -1,0 +1,220 @@
+"""ctypes binding of include/yy.h (names follow the C ABI one to one).
+
+Marshalling only: shapes are checked, arrays are made C-contiguous fp64 and
+handed to libyy.so.  Device memory, kernels and the Schwarz loop live in the
+library.  See include/yy.h for argument meaning, layout and errors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int32, c_void_p
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+YY_OK, YY_ENOCONV = 0, 4
+YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS = 1, 2, 3
+TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
+
+EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
+           "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_time",
+           "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve")
+
+
+class YYError(RuntimeError):
+    pass
+
+
+class yy_grid(ctypes.Structure):
+    _fields_ = [("nr", c_int32), ("ntheta", c_int32), ("nphi", c_int32)]
+
+
+_DP = POINTER(c_double)
+
+
+class yy_fields(ctypes.Structure):
+    _fields_ = [("ur", _DP), ("ut", _DP), ("up", _DP), ("p", _DP), ("T", _DP)]
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libyy.so")
+
+
+_lib = None
+
+
+def load_library():
+    """Load libyy.so (in-tree).  Raises YYError if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = lib_path()
+    if not os.path.exists(p):
+        raise YYError(f"{p} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(p)
+    ctx = c_void_p
+    L.yy_create.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double, POINTER(ctx)]
+    L.yy_set_fields.argtypes = [ctx, c_int32, c_int32, c_int32, POINTER(yy_fields)]
+    L.yy_get_fields.argtypes = [ctx, c_int32, c_int32, c_int32, POINTER(yy_fields)]
+    L.yy_set_wall.argtypes = [ctx, c_int32, c_int32, POINTER(c_int32), POINTER(yy_fields)]
+    L.yy_set_source.argtypes = [ctx, c_int32, c_int32, POINTER(c_int32), POINTER(yy_fields)]
+    L.yy_set_param.argtypes = [ctx, c_int32, c_double]
+    L.yy_set_stream.argtypes = [ctx, c_void_p]
+    L.yy_step.argtypes = [ctx, c_int32, c_double]
+    L.yy_get_stats.argtypes = [ctx, c_int32, POINTER(c_int32), POINTER(c_double), POINTER(c_int32)]
+    L.yy_time.argtypes = [ctx]
+    L.yy_time.restype = c_double
+    L.yy_last_error.argtypes = [ctx]
+    L.yy_last_error.restype = c_char_p
+    L.yy_destroy.argtypes = [ctx]
+    L.yy_destroy.restype = None
+    L.yy_debug_get.argtypes = [ctx, c_char_p, c_int32, _DP]
+    L.yy_line_solve.argtypes = [ctx, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
+    for name in ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
+                 "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve"):
+        getattr(L, name).restype = c_int32
+    _lib = L
+    return L
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_DP) if a is not None else None
+
+
+class Shell:
+    """One Yin-Yang shell context (include/yy.h `yy_ctx`)."""
+
+    def __init__(self, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3,
+                 chi=None, max_iters=None, fixed_iters=None, stream=None):
+        self.L = load_library()
+        self.nr, self.nt, self.np_ = nr, ntheta, nphi
+        g = yy_grid(nr, ntheta, nphi)
+        h = c_void_p()
+        st = self.L.yy_create(ctypes.byref(g), R1, R2, Pr, Ra, dt, ctypes.byref(h))
+        if st != YY_OK:
+            raise YYError(f"yy_create failed with status {st}")
+        self.h = h
+        if chi is not None:
+            self.set_param(YY_CHI, chi)
+        if max_iters is not None:
+            self.set_param(YY_MAX_ITERS, max_iters)
+        if fixed_iters is not None:
+            self.set_param(YY_FIXED_ITERS, fixed_iters)
+        if stream is not None:
+            self.set_stream(stream)
+
+    # shapes of include/yy.h
+    def shape(self, name):
+        nr, nt, npp = self.nr, self.nt, self.np_
+        return {"ur": (nr + 1, nt, npp), "ut": (nr, nt + 1, npp), "up": (nr, nt, npp + 1),
+                "p": (nr, nt, npp), "T": (nr, nt, npp)}[name]
+
+    def wall_shape(self, name):
+        return (2,) + self.shape(name)[1:]
+
+    def _check(self, st, what):
+        if st < 0:
+            msg = self.L.yy_last_error(self.h).decode(errors="replace")
+            raise YYError(f"{what}: status {st}: {msg}")
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.yy_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def set_param(self, key, value):
+        self._check(self.L.yy_set_param(self.h, key, float(value)), "yy_set_param")
+
+    def set_stream(self, stream):
+        """stream: an int cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(self.L.yy_set_stream(self.h, c_void_p(int(stream))), "yy_set_stream")
+
+    def _fields(self, arrays, shape_fn):
+        keep = {}
+        f = yy_fields()
+        for name in ("ur", "ut", "up", "p", "T"):
+            a = arrays.get(name)
+            if a is None:
+                continue
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            if a.shape != shape_fn(name):
+                raise YYError(f"{name}: shape {a.shape} != {shape_fn(name)}")
+            keep[name] = a
+            setattr(f, name, _ptr(a))
+        return f, keep
+
+    def set_fields(self, patch, level, system, **arrays):
+        f, keep = self._fields(arrays, self.shape)
+        self._check(self.L.yy_set_fields(self.h, patch, level, system, ctypes.byref(f)), "yy_set_fields")
+
+    def get_fields(self, patch, level=0, system=2, names=("ur", "ut", "up", "p", "T")):
+        out = {n: np.empty(self.shape(n)) for n in names if not (n == "p" and level == 1)}
+        f = yy_fields()
+        for n, a in out.items():
+            setattr(f, n, _ptr(a))
+        self._check(self.L.yy_get_fields(self.h, patch, level, system, ctypes.byref(f)), "yy_get_fields")
+        return out
+
+    def _terms(self, fn, patch, terms, shape_fn, what):
+        n = len(terms)
+        tfs = (c_int32 * max(n, 1))(*[int(t) for t, _ in terms])
+        arr = (yy_fields * max(n, 1))()
+        keep = []
+        for m, (_, d) in enumerate(terms):
+            f, k = self._fields(d, shape_fn)
+            arr[m] = f
+            keep.append(k)
+        self._check(fn(self.h, patch, n, tfs, arr), what)
+
+    def set_wall(self, patch, terms):
+        """terms: [(timefn, {"T","ur","ut","up": (2, ., .) arrays})]"""
+        self._terms(self.L.yy_set_wall, patch, terms, self.wall_shape, "yy_set_wall")
+
+    def set_source(self, patch, terms):
+        """terms: [(timefn, {"T","ur","ut","up": full 3-D arrays})]"""
+        self._terms(self.L.yy_set_source, patch, terms, self.shape, "yy_set_source")
+
+    def step(self, nsteps=1, tol=1e-10):
+        return self._check(self.L.yy_step(self.h, int(nsteps), float(tol)), "yy_step")
+
+    def stats(self, cap=100000):
+        it = (c_int32 * cap)()
+        rs = (c_double * cap)()
+        n = c_int32()
+        self._check(self.L.yy_get_stats(self.h, cap, it, rs, ctypes.byref(n)), "yy_get_stats")
+        return [(it[q], rs[q]) for q in range(n.value)]
+
+    def time(self):
+        return self.L.yy_time(self.h)
+
+    def debug_get(self, name, patch):
+        kind = {"astar_r": "ur", "astar_t": "ut", "astar_p": "up", "G_T": "T"}.get(name)
+        if kind is None:
+            kind = name[2:4]
+        out = np.empty(self.shape(kind))
+        self._check(self.L.yy_debug_get(self.h, name.encode(), patch, _ptr(out)), "yy_debug_get")
+        return out
+
+    def line_solve(self, axis, ar, at, ap, x):
+        """C4 kernel-only sweep on device tensors (torch, float64, contiguous)."""
+        for t in (ar, at, ap, x):
+            if not (t.is_cuda and t.dtype.is_floating_point and t.is_contiguous()):
+                raise YYError("line_solve needs contiguous CUDA float64 tensors")
+        self._check(self.L.yy_line_solve(self.h, axis, c_void_p(ar.data_ptr()), c_void_p(at.data_ptr()),
+                                         c_void_p(ap.data_ptr()), c_void_p(x.data_ptr())), "yy_line_solve")
+
+    def load_workload(self, wl):
+        """Upload a workloads.make_workload() dict (levels, walls, sources)."""
+        for patch, pd in enumerate(wl["patches"]):
+            n = pd["n"]
+            self.set_fields(patch, 0, 1, ur=n["ur"], ut=n["ut"], up=n["up"], T=n["T"], p=n["p1"])
+            self.set_fields(patch, 0, 2, ur=n["ur"], ut=n["ut"], up=n["up"], p=n["p2"])
+            m = pd["nm1"]
+            self.set_fields(patch, 1, 0, **{k: m[k] for k in ("ur", "ut", "up", "T")})
+            self.set_wall(patch, pd["walls"])
+            self.set_source(patch, pd["sources"])

@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path (through the C ABI, paper_1905_02300_b200.Shell)
+against the CPU oracle on the same seeded inputs, element by element.
+
+Bar (BASELINE.json north_star): max relative error <= 1e-11 per step, per
+field as ||gpu - oracle||_inf / ||oracle||_inf, and identical Schwarz
+iteration counts.  Sizes span several 128-wide thread blocks with ragged
+tails; full BASELINE sizes are covered in test_gpu_fullsize.py."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle.scheme import Oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-11
+
+
+def _shell(cfg, **kw):
+    from paper_1905_02300_b200 import Shell
+    return Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, **kw)
+
+
+def _oracle(cfg, **kw):
+    return Oracle(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, **kw)
+
+
+def _relerr(sh, o):
+    """max over patches, systems, levels and fields of ||gpu - oracle||_inf /
+    ||oracle||_inf, where the velocity components share the norm of their
+    vector (max over u_r, u_th, u_ph of that system and level) — DESIGN.md
+    'Parity metric'."""
+    worst = 0.0
+    where = None
+    for p in range(2):
+        for s in (1, 2):
+            for lev in (0, 1):
+                a = sh.get_fields(p, lev, s)
+                b = o.get_fields(p, lev, s)
+                vmax = max(np.max(np.abs(b[q])) for q in ("ur", "ut", "up"))
+                for k in a:
+                    den = vmax if k in ("ur", "ut", "up") else np.max(np.abs(b[k]))
+                    den = max(den, 1e-300)
+                    e = float(np.max(np.abs(a[k] - b[k])) / den)
+                    if e > worst:
+                        worst, where = e, (p, s, lev, k)
+    return worst, where
+
+
+def _pair(cfg, steps, wl=None, tol=None, oracle_kw=None, shell_kw=None):
+    wl = wl if wl is not None else W.make_workload(cfg)
+    tol = cfg.tol if tol is None else tol
+    sh = _shell(cfg, **(shell_kw or {}))
+    sh.load_workload(wl)
+    o = _oracle(cfg, **(oracle_kw or {}))
+    o.load_workload(wl)
+    errs = []
+    for _ in range(steps):
+        sh.step(1, tol)
+        o.step(1, tol)
+        e, where = _relerr(sh, o)
+        errs.append(e)
+        assert e <= TOL_STEP, (e, where)
+        assert sh.stats()[-1][0] == o.stats[-1][0], (sh.stats(), o.stats)
+    return sh, o, errs
+
+
+def test_c1_manufactured_three_steps():
+    _pair(W.config("C1"), 3)
+
+
+def test_ragged_random_state():
+    # odd sizes: ragged 128-wide blocks in every launch; noisy levels so every
+    # stencil weight and fringe value matters
+    cfg = W.small("C1", 7, 13, 37, Ra=30.0, dt=2e-3)
+    _pair(cfg, 2, wl=W.random_state(cfg, seed=11, amp=5.0))
+
+
+def test_convection_reduced():
+    cfg = W.small("C3", 10, 18, 50)
+    _pair(cfg, 2)
+
+
+def test_landau_reduced():
+    cfg = W.small("C2", 8, 16, 45)
+    _pair(cfg, 2)
+
+
+def test_wide_phi_rows():
+    # nphi - 2 = 129 unknowns per phi-line: two blocks in x, one nearly empty
+    cfg = W.small("C1", 3, 10, 131, dt=1e-3)
+    _pair(cfg, 1)
+
+
+def test_fixed_iterations_mode():
+    cfg = W.small("C1", 5, 12, 30, dt=1e-3)
+    _pair(cfg, 2, oracle_kw={"fixed_iters": 3}, shell_kw={"fixed_iters": 3})
+
+
+def test_static_rhs_parity():
+    # O2/O3 stage alone: a* and the seven G_q arrays of the first step
+    cfg = W.small("C1", 6, 14, 33, Ra=50.0, dt=2e-3)
+    wl = W.random_state(cfg, seed=3, amp=3.0)
+    sh = _shell(cfg, fixed_iters=1)
+    sh.load_workload(wl)
+    sh.step(1, 1e-10)
+    o = _oracle(cfg)
+    o.load_workload(wl)
+    for p in range(2):
+        astar, G = o.static(p, 0.0)
+        for name, ref in zip(("astar_r", "astar_t", "astar_p"), astar):
+            assert np.max(np.abs(sh.debug_get(name, p) - ref)) <= 1e-14 * np.max(np.abs(ref))
+        for q in ("T", "ur1", "ut1", "up1", "ur2", "ut2", "up2"):
+            kind = {"T": "C", "u": None}.get(q[0]) or {"r": "R", "t": "TH", "p": "PH"}[q[1]]
+            m = o.g.solved_mask(kind)
+            a = sh.debug_get("G_" + q, p)[m]
+            b = G[q][m]
+            assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b)), q
+
+
+def test_deterministic_bitwise():
+    cfg = W.small("C1", 5, 12, 30, dt=1e-3)
+    wl = W.random_state(cfg, seed=5)
+    out = []
+    for _ in range(2):
+        sh = _shell(cfg)
+        sh.load_workload(wl)
+        sh.step(2, 1e-10)
+        out.append([sh.get_fields(p, 0, 2) for p in range(2)])
+        st = sh.stats()
+    for p in range(2):
+        for k in out[0][p]:
+            assert np.array_equal(out[0][p][k], out[1][p][k])
+
+
+def test_line_solve_c4_reduced():
+    import torch
+    from oracle import ops
+    nr, nt, npp = 9, 21, 67
+    a, rhs = W.c4_inputs(nr, nt, npp)
+    cfg = W.Config("C4", nr, nt, npp, dt=1e-4)
+    sh = _shell(cfg)
+    o = _oracle(cfg)
+    astar = [a["ur"], a["ut"], a["up"]]
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    for axis in range(3):
+        x = dev(rhs)
+        sh.line_solve(axis, dev(a["ur"]), dev(a["ut"]), dev(a["up"]), x)
+        torch.cuda.synchronize()
+        got = x.cpu().numpy()
+        ref = o.sweep("T", rhs, axis, ops.coeffs(o.g, o.prm, "T", axis, True, astar))
+        m = o.g.solved_mask("C")
+        assert np.max(np.abs(got[m] - ref[m])) <= 1e-13 * np.max(np.abs(ref[m])), axis
+
+
+def test_errors_are_reported():
+    from paper_1905_02300_b200 import YYError
+    cfg = W.small("C1", 4, 12, 28)
+    sh = _shell(cfg)
+    with pytest.raises(YYError):
+        sh.set_fields(2, 0, 0, T=np.zeros((4, 12, 28)))
+    with pytest.raises(YYError):
+        sh.set_param(99, 1.0)
+    with pytest.raises(YYError):
+        sh.step(1, -1.0)

@@ -259,8 +259,8 @@ def _sample_vector(cfg, patch, fn):
 
 def _sample_scalar(cfg, patch, fn, kind="C"):
     r, th, ph, x, y, z, basis = node_grid(cfg, patch, kind)
-    return np.ascontiguousarray(np.broadcast_to(fn(x, y, z), (len(r), th.shape[1], ph.shape[2])),
-                                dtype=np.float64)
+    return np.array(np.broadcast_to(fn(x, y, z), (len(r), th.shape[1], ph.shape[2])),
+                    dtype=np.float64, order="C", copy=True)
 
 
 def _sample_walls_vector(cfg, patch, fn):
@@ -286,8 +286,8 @@ def _sample_walls_scalar(cfg, patch, fn):
     rw = np.array([cfg.R1, cfg.R2])[:, None, None]
     x, y, z = chart_xyz(patch, rw, th, ph)
     shape = (2, len(t1), len(p1))
-    return np.ascontiguousarray(np.broadcast_to(fn(*(np.broadcast_to(v, shape) for v in (x, y, z))), shape),
-                                dtype=np.float64)
+    return np.array(np.broadcast_to(fn(*(np.broadcast_to(v, shape) for v in (x, y, z))), shape),
+                    dtype=np.float64, order="C", copy=True)
 
 
 def make_workload(cfg: Config):
