@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py — full Yin-Yang AC direction-splitting time steps on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl yy|reference] [--workload C3]
+
+One "step" = one full time step of the paper's method (SURVEY.md §8(a) rows
+a1-a9: static RHS, additive Schwarz iterated to tol with splitting-error
+reduction, pressure updates) on both Yin-Yang patches of the workload.
+Prints ONE JSON line (rank 0).  Metric: cell-updates/s = 2 patches x cells
+per patch x steps / device time (BASELINE.json metric); inputs larger than L2
+(the C3 working set is ~2.8 GB), so no flush is needed between steps.
+
+--impl reference runs the CPU oracle (oracle/, plain numpy fp64) on a bounded
+sample of the same workload (full time steps on a 1/64-cell copy of it).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "full time steps: cell-updates/s and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "cell-updates/s"
+HBM_NOMINAL_GBS = 8000.0          # BASELINE.json roofline denominator (8 TB/s)
+SAMPLE_DIV = {"C1": 1, "C2": 2, "C3": 4, "C5": 4}   # CPU sample grid = workload grid / d per axis
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------------
+# algorithmic bytes (SURVEY.md §8(d) model M1: each pass reads each input array
+# once and writes each output once, 8 B per value; halos and 1-D tables free)
+# ---------------------------------------------------------------------------------
+def kind_nodes(cfg, kind):
+    nr, nt, npp = cfg.nr, cfg.nth, cfg.nph
+    return {"C": nr * nt * npp, "R": (nr + 1) * nt * npp, "TH": nr * (nt + 1) * npp,
+            "PH": nr * nt * (npp + 1)}[kind]
+
+
+QK = {"T": "C", "ur": "R", "ut": "TH", "up": "PH"}
+
+
+def m1_bytes(name, cfg, nsrc):
+    """Algorithmic bytes of ONE launch of kernel class `name` (both patches)."""
+    P = 2
+    if name.startswith("sweep_"):
+        _, q, ax = name.split("_")[:3]
+        fin = name.endswith("_fin")
+        extra = 0
+        if q == "ut" and ax == "th":
+            extra = 1          # reaction -(a_r/r) u reads a*_r
+        if q == "up" and ax == "ph":
+            extra = 2          # reaction reads a*_r, a*_th
+        arrays = 1 + 1 + extra + 1 + (1 if fin else 0)   # rhs, a*_ax, extras, write, (+psi read)
+        return 8 * P * kind_nodes(cfg, QK[q]) * arrays
+    if name.startswith("resid_"):
+        q = name[6:8] if name[6:8] in ("ur", "ut", "up") else "T"
+        s = name[-1]
+        ins = {"T": 0, "ur": 2, "ut": 2, "up": 4}[q] + (2 if (q != "T" and s == "2") else 0)
+        return 8 * P * kind_nodes(cfg, QK[q]) * (6 + ins + 1)
+    if name.startswith("static_"):
+        q = name[7:]
+        reads = {"T": 5, "ur": 17, "ut": 13, "up": 9}[q] + nsrc
+        writes = 1 if q == "T" else 2
+        return 8 * P * kind_nodes(cfg, QK[q]) * (reads + writes)
+    if name.startswith("pres_"):
+        return 8 * P * kind_nodes(cfg, "C") * (8 + (2 if name.endswith("2") else 0) + 1)
+    if name == "astar":
+        return 8 * P * kind_nodes(cfg, "R") * 3
+    return 0
+
+
+def step_model_bytes(cfg, K, forced):
+    """M1 bytes of one full step with K Schwarz iterations."""
+    per_cell = (352 if forced else 256) + 1320 * K
+    return 2 * cfg.cells * per_cell
+
+
+# ---------------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------------
+def oracle_sample_step(cfg_name):
+    """One complete time step of the workload's physics on a 1/d^3-cell copy of
+    its grid, by the plain numpy oracle.  Returns (cells, seconds, K)."""
+    import workloads as W
+    from oracle.scheme import Oracle
+    full = W.config(cfg_name)
+    d = SAMPLE_DIV[cfg_name]
+    c = W.small(cfg_name, full.nr // d, full.nth // d, full.nph // d)
+    o = Oracle(c.nr, c.nth, c.nph, c.R1, c.R2, c.Pr, c.Ra, c.dt)
+    o.load_workload(W.make_workload(c))
+    t0 = time.perf_counter()
+    o.step(1, c.tol)
+    dt = time.perf_counter() - t0
+    return 2 * c.cells, dt, o.stats[-1][0], (c.nr, c.nth, c.nph)
+
+
+def cpu_cores_used():
+    return 1   # numpy elementwise kernels run single-threaded (no BLAS in the oracle step)
+
+
+# ---------------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    steps = []
+    for i in range(args.warmup + args.steps):
+        cells, sec, K, grid = oracle_sample_step(args.workload)
+        if i >= args.warmup:
+            steps.append((cells, sec, K))
+    tot_cells = sum(s[0] for s in steps)
+    tot_sec = sum(s[1] for s in steps)
+    v = tot_cells / tot_sec
+    sample = (f"{args.workload} physics on a {grid[0]}x{grid[1]}x{grid[2]} per-patch grid (1/{SAMPLE_DIV[args.workload] ** 3} "
+              f"of the cells), one full time step per bench step, mean Schwarz K={statistics.mean(s[2] for s in steps):.1f}")
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_sec / len(steps),
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic", "config": {"workload": args.workload, "sample": sample},
+          "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle", "sample": sample},
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    return 0
+
+
+def run_yy(args):
+    import numpy as np
+    import torch
+
+    import workloads as W
+    from paper_1905_02300_b200 import Shell
+
+    rank, world, local = dist_env()
+    if world > 1:
+        if rank == 0:
+            emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                  "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                  "dtype": "f64", "data": "synthetic", "config": {"workload": "C5"},
+                  "error": "multi-GPU layout (Yin/Yang x radial slabs, NCCL) not built yet; N=1 only"})
+        return 0
+    torch.cuda.set_device(local)
+    cfg = W.config(args.workload)
+    wl = W.make_workload(cfg)
+    nsrc = len(wl["patches"][0]["sources"])
+    forced = nsrc > 0
+    stream = torch.cuda.Stream()
+    sh = Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, stream=stream.cuda_stream)
+    sh.load_workload(wl)
+    W_ = max(3, args.warmup)
+    for _ in range(W_):
+        sh.step(1, cfg.tol)
+    torch.cuda.synchronize()
+    sh.profile(True)
+    l0 = sh.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    sh.step(args.steps, cfg.tol)
+    ev1.record(stream)
+    ev1.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = sh.launch_count() - l0
+    prof = sh.profile_report()
+    sh.profile(False)
+    stats = sh.stats()[-args.steps:]
+    Ks = [k for k, _ in stats]
+    cells = 2 * cfg.cells
+    value = cells * args.steps / (ms / 1e3)
+    peak, peak_kind = measured_peak()
+    # dominant kernel class
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    dname, (dcount, dms) = dom
+    dbytes = m1_bytes(dname, cfg, nsrc)
+    davg_s = dms / dcount / 1e3
+    achieved = dbytes / davg_s / 1e9 if dbytes else None
+    share = dms / ms
+    # whole-step model roofline
+    model_bytes = sum(step_model_bytes(cfg, k, forced) for k in Ks)
+    t_roof_8 = model_bytes / (HBM_NOMINAL_GBS * 1e9)
+    t_roof_m = model_bytes / (peak * 1e9)
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        def pinned(a):
+            t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+            t.numpy()[...] = a
+            return t.numpy()
+        host = []
+        h2d = 0
+        for pd in wl["patches"]:
+            n, m = pd["n"], pd["nm1"]
+            d = {"n1": {k: pinned(n[k]) for k in ("ur", "ut", "up", "T")},
+                 "p1": pinned(n["p1"]), "p2": pinned(n["p2"]),
+                 "m": {k: pinned(m[k]) for k in ("ur", "ut", "up", "T")}}
+            u_b = sum(d["n1"][k].nbytes for k in ("ur", "ut", "up"))
+            # yy_set_fields copies: level 0 system 1 (u, T, p1), level 0 system 2 (u, p2),
+            # level 1 system 0 (u twice: both systems, T once)
+            h2d += u_b + d["n1"]["T"].nbytes + d["p1"].nbytes
+            h2d += u_b + d["p2"].nbytes
+            h2d += 2 * u_b + d["m"]["T"].nbytes
+            host.append(d)
+        outs = [{k: pinned(np.zeros(sh.shape(k))) for k in ("ur", "ut", "up", "p", "T")} for _ in range(2)]
+        d2h = sum(v.nbytes for o in outs for v in o.values())
+        from paper_1905_02300_b200.yy import _ptr, yy_fields
+        import ctypes
+
+        def upload_step_download():
+            for p, d in enumerate(host):
+                sh.set_fields(p, 0, 1, ur=d["n1"]["ur"], ut=d["n1"]["ut"], up=d["n1"]["up"], T=d["n1"]["T"], p=d["p1"])
+                sh.set_fields(p, 0, 2, ur=d["n1"]["ur"], ut=d["n1"]["ut"], up=d["n1"]["up"], p=d["p2"])
+                sh.set_fields(p, 1, 0, **d["m"])
+            sh.step(1, cfg.tol)
+            for p in range(2):
+                f = yy_fields()
+                for k, a in outs[p].items():
+                    setattr(f, k, _ptr(a))
+                sh._check(sh.L.yy_get_fields(sh.h, p, 0, 2, ctypes.byref(f)), "yy_get_fields")
+        upload_step_download()          # warm
+        ne = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            upload_step_download()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / ne
+        e2e = {"value": cells / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
+               "schwarz_iters": sh.stats()[-1][0], "timing": "host perf_counter, device synchronised"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        c_cells, c_sec, c_K, grid = oracle_sample_step(args.workload)
+        cpu = {"value": c_cells / c_sec, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
+               "sample": f"one full time step of {args.workload} physics on a {grid[0]}x{grid[1]}x{grid[2]} "
+                         f"per-patch grid (1/{SAMPLE_DIV[args.workload] ** 3} of the cells), Schwarz K={c_K}, {c_sec:.1f} s"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": W_,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
+                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra, "schwarz_tol": cfg.tol,
+                   "schwarz_iters_per_step": Ks, "l2_flush": "inputs larger than L2 (working set ~37 fp64 fields)",
+                   "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
+                                     "model_bytes": model_bytes,
+                                     "frac_of_8TBs": t_roof_8 / (ms / 1e3),
+                                     "frac_of_measured_hbm": t_roof_m / (ms / 1e3)}},
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "peak_source": peak_kind, "bytes_per_launch": dbytes, "avg_launch_ms": davg_s * 1e3,
+                     "launches": dcount, "share_of_step": share},
+        "kernel_classes": {k: {"launches": n, "ms": t, "GBps": (m1_bytes(k, cfg, nsrc) * n / (t / 1e3) / 1e9)
+                               if t > 0 and m1_bytes(k, cfg, nsrc) else None}
+                           for k, (n, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    emit(out)
+    sh.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="yy", choices=("yy", "reference"))
+    ap.add_argument("--workload", default="C3", choices=("C1", "C2", "C3", "C5"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_yy(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -61,7 +61,8 @@ enum { YY_TF_ONE = 0, YY_TF_COS = 1, YY_TF_SIN = 2, YY_TF_COS2 = 3 };
 enum {
   YY_CHI = 1,          /* artificial-compressibility chi (eq:ac1); default 1 (RD19) */
   YY_MAX_ITERS = 2,    /* Schwarz K_max (RD25); default 100                                  */
-  YY_FIXED_ITERS = 3   /* >0: run exactly this many iterations per step, ignore tol          */
+  YY_FIXED_ITERS = 3,  /* >0: run exactly this many iterations per step, ignore tol          */
+  YY_PROFILE = 4       /* !=0: time every kernel class with CUDA events (resets the table)   */
 };
 
 typedef struct {
@@ -120,6 +121,13 @@ yy_status yy_get_stats(const yy_ctx* ctx, int32_t cap, int32_t* iters_per_step,
                        double* resid_per_step, int32_t* n_out);
 
 double yy_time(const yy_ctx* ctx);
+
+/* Number of CUDA kernels this context has launched since creation. */
+int64_t yy_launch_count(const yy_ctx* ctx);
+
+/* Per-kernel-class device time since YY_PROFILE was set: one line per class,
+ * "name launches total_ms\n", written to buf (len bytes, NUL-terminated). */
+yy_status yy_profile_report(yy_ctx* ctx, char* buf, int32_t len);
 const char* yy_last_error(const yy_ctx* ctx);
 void yy_destroy(yy_ctx* ctx);   /* NULL is a no-op */
 

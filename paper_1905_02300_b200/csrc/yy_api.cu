@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -70,6 +71,14 @@ struct yy_ctx {
   VecTab tth{}, tph{};
   std::vector<int> st_iters;
   std::vector<double> st_rho;
+  // instrumentation: kernel launch counter (always on) and an optional
+  // CUDA-event profiler per kernel class (YY_PROFILE)
+  long long launches = 0;
+  bool prof_on = false;
+  struct Rec { const char* name; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  std::map<std::string, std::pair<long long, double>> prof;
 };
 
 namespace {
@@ -101,6 +110,62 @@ yy_status dalloc(yy_ctx* ctx, T** p, size_t count) {
     yy_status s_ = (x);             \
     if (s_ != YY_OK) return s_;     \
   } while (0)
+
+// ---- instrumentation ----------------------------------------------------------------
+cudaEvent_t ev_get(yy_ctx* ctx) {
+  if (!ctx->pool.empty()) {
+    cudaEvent_t e = ctx->pool.back();
+    ctx->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {   // brackets one or more launches of one kernel class
+  yy_ctx* ctx;
+  yy_ctx::Rec r{};
+  ProfScope(yy_ctx* c, const char* name, int nlaunch) : ctx(c) {
+    ctx->launches += nlaunch;
+    if (ctx->prof_on) {
+      r.name = name;
+      r.a = ev_get(ctx);
+      r.b = ev_get(ctx);
+      cudaEventRecord(r.a, ctx->st);
+    }
+  }
+  ~ProfScope() {
+    if (ctx->prof_on) {
+      cudaEventRecord(r.b, ctx->st);
+      ctx->pending.push_back(r);
+    }
+  }
+};
+
+void prof_collect(yy_ctx* ctx) {   // call after a stream synchronisation
+  for (auto& r : ctx->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& e = ctx->prof[r.name];
+    e.first += 1;
+    e.second += ms;
+    ctx->pool.push_back(r.a);
+    ctx->pool.push_back(r.b);
+  }
+  ctx->pending.clear();
+}
+
+const char* QNAME[4] = {"T", "ur", "ut", "up"};
+const char* AXNAME[3] = {"r", "th", "ph"};
+std::string g_names_store[512];
+const char* kname(const std::string& s) {   // interned kernel-class names
+  for (auto& x : g_names_store) {
+    if (x == s) return x.c_str();
+    if (x.empty()) { x = s; return x.c_str(); }
+  }
+  return "other";
+}
 
 // ---- geometry (reading RD1/RD2; §2) --------------------------------------
 struct HostGeo {
@@ -271,6 +336,7 @@ yy_status eval_walls(yy_ctx* ctx, int L, double t) {
           in.c[nin] = tf_value(ctx->wtf[p][m], t);
           ++nin;
         }
+      ProfScope ps(ctx, "walls", 1);
       launch_lincomb(ctx->wl[L][f] + p * ws, ws, in, nin, ctx->st);
     }
   }
@@ -328,7 +394,10 @@ yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
   r.urit = ctx->it[FUR1 + o]; r.urn = ctx->n[FUR1 + o];
   r.utit = ctx->it[FUT1 + o]; r.utn = ctx->n[FUT1 + o];
   r.p1it = ctx->it[FP1]; r.p1n = ctx->n[FP1];
-  launch_resid(g, q, s, r, ctx->st);
+  {
+    ProfScope ps(ctx, kname(std::string("resid_") + QNAME[q] + (q ? (s == 1 ? "1" : "2") : "")), 1);
+    launch_resid(g, q, s, r, ctx->st);
+  }
   SweepArgs w{};
   w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
   w.R = ctx->R; w.C = ctx->C; w.psi = ctx->it[f];
@@ -336,6 +405,7 @@ yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
   w.maxb = ctx->maxb;
   for (int a = 0; a < 3; ++a) {
     const bool fin = (a == 2);
+    ProfScope ps(ctx, kname(std::string("sweep_") + QNAME[q] + "_" + AXNAME[ORDER[q][a]] + (fin ? "_fin" : "")), 1);
     const int nb = launch_sweep(g, q, ORDER[q][a], fin, w, 2, ctx->st);
     if (fin) nblk[slot] = nb;
   }
@@ -353,16 +423,20 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
     LinIn in{};
     in.p[0] = ctx->n[FUR2 + c]; in.c[0] = 1.5;
     in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
+    ProfScope ps(ctx, "astar", 1);
     launch_lincomb(ctx->astar[c], 2 * fsize(ctx, FUR2 + c), in, 2, st);
   }
   // O3: static right-hand sides
   for (int q = 0; q < 4; ++q) {
     StaticArgs a = static_args(ctx, q, t + 0.5 * tau);
+    ProfScope ps(ctx, kname(std::string("static_") + QNAME[q]), 1);
     launch_static(g, q, a, st);
   }
   // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
-  for (int f = 0; f < NF; ++f)
+  for (int f = 0; f < NF; ++f) {
+    ProfScope ps(ctx, "copy_iterate", 0);
     CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], 2 * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
   const long long plane = (long long)g.nt * g.np;
   for (int f : {FUR1, FUR2})
     for (int p = 0; p < 2; ++p)
@@ -383,7 +457,10 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
   ra.maxb = ctx->maxb;
   while (k < kmax) {
     ++k;
-    launch_interp(g, ia, st);                              // O5
+    {
+      ProfScope ps(ctx, "interp", 3);
+      launch_interp(g, ia, st);                            // O5
+    }
     TRY(solve_quantity(ctx, QT, 1, 0, ra.nblk));           // O6
     for (int s = 1; s <= 2; ++s) {                         // O7 / O9
       const int base = (s == 1) ? 1 : 5;
@@ -400,12 +477,17 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
       pa.pit = ctx->it[s == 1 ? FP1 : FP2];
       pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
       pa.maxb = ctx->maxb;
+      ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
       ra.nblk[base + 3] = launch_pres(g, s, pa, st);
     }
-    launch_reduce(ctx->part, ra, ctx->red, st);            // O10
+    {
+      ProfScope ps(ctx, "reduce", 1);
+      launch_reduce(ctx->part, ra, ctx->red, st);          // O10
+    }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (ctx->prof_on) prof_collect(ctx);
     rho = ctx->red_host[0];
     if (ctx->red_host[1] != 0.0) return fail(ctx, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
     if (ctx->fixed_iters <= 0 && rho < tol) break;
@@ -595,6 +677,12 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       if (v < 0) return fail(ctx, YY_EINVAL, "fixed_iters must be >= 0");
       ctx->fixed_iters = (int)v;
       return YY_OK;
+    case YY_PROFILE:
+      cudaStreamSynchronize(ctx->st);
+      prof_collect(ctx);
+      ctx->prof.clear();
+      ctx->prof_on = v != 0;
+      return YY_OK;
   }
   return fail(ctx, YY_EINVAL, "unknown parameter key");
 }
@@ -634,6 +722,22 @@ yy_status yy_get_stats(const yy_ctx* ctx, int32_t cap, int32_t* iters, double* r
 }
 
 double yy_time(const yy_ctx* ctx) { return ctx ? ctx->t : 0.0; }
+
+int64_t yy_launch_count(const yy_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+yy_status yy_profile_report(yy_ctx* ctx, char* buf, int32_t len) {
+  if (!ctx || !buf || len <= 0) return YY_EINVAL;
+  cudaStreamSynchronize(ctx->st);
+  prof_collect(ctx);
+  std::string out;
+  for (auto& kv : ctx->prof) {
+    char line[160];
+    std::snprintf(line, sizeof line, "%s %lld %.6f\n", kv.first.c_str(), kv.second.first, kv.second.second);
+    out += line;
+  }
+  std::snprintf(buf, (size_t)len, "%s", out.c_str());
+  return (int32_t)out.size() < len ? YY_OK : YY_EINVAL;
+}
 
 const char* yy_last_error(const yy_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
 

@@ -15,12 +15,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 YY_OK, YY_ENOCONV = 0, 4
-YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS = 1, 2, 3
+YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE = 1, 2, 3, 4
 TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
            "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_time",
-           "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve")
+           "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve", "yy_launch_count",
+           "yy_profile_report")
 
 
 class YYError(RuntimeError):
@@ -72,8 +73,12 @@ def load_library():
     L.yy_destroy.restype = None
     L.yy_debug_get.argtypes = [ctx, c_char_p, c_int32, _DP]
     L.yy_line_solve.argtypes = [ctx, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
+    L.yy_launch_count.argtypes = [ctx]
+    L.yy_launch_count.restype = ctypes.c_int64
+    L.yy_profile_report.argtypes = [ctx, ctypes.c_char_p, c_int32]
     for name in ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
-                 "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve"):
+                 "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve",
+                 "yy_profile_report"):
         getattr(L, name).restype = c_int32
     _lib = L
     return L
@@ -191,6 +196,22 @@ class Shell:
 
     def time(self):
         return self.L.yy_time(self.h)
+
+    def launch_count(self):
+        return int(self.L.yy_launch_count(self.h))
+
+    def profile(self, on=True):
+        self.set_param(YY_PROFILE, 1.0 if on else 0.0)
+
+    def profile_report(self):
+        """{kernel class: (launches, total_ms)} since profile(True)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        self._check(self.L.yy_profile_report(self.h, buf, len(buf)), "yy_profile_report")
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, n, ms = line.split()
+            out[name] = (int(n), float(ms))
+        return out
 
     def debug_get(self, name, patch):
         kind = {"astar_r": "ur", "astar_t": "ut", "astar_p": "up", "G_T": "T"}.get(name)
