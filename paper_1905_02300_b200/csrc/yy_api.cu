@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <string>
@@ -531,23 +532,69 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   g.cchi = 1.0 / (2.0 * ctx->chi); g.inv_chi = 1.0 / ctx->chi; g.PrRa = Pr * Ra;
   const double th1 = M_PI / 4 - 2.0 * h.dth;   // RD31
   g.hatph = 1.0 / (R1 * R1 * std::sin(th1) * std::sin(th1) * h.dph * h.dph);
-  // 1-D tables
+  // 1-D coordinate and factor tables (SURVEY Appendix A rows as products of
+  // 1-D factors; computed once here in fp64, so no kernel divides)
+  const int nr = h.nr, nt = h.nt;
+  const double dr = h.dr, dth = h.dth;
+  std::vector<double> rc(nr), rf(nr + 1), sc(nt), sf(nt + 1), cc(nt), cf(nt + 1);
+  for (int i = 0; i < nr; ++i) rc[i] = R1 + (i + 0.5) * dr;
+  for (int i = 0; i <= nr; ++i) rf[i] = R1 + i * dr;
+  for (int j = 0; j < nt; ++j) { sc[j] = std::sin(h.th0 + (j + 0.5) * dth); cc[j] = std::cos(h.th0 + (j + 0.5) * dth); }
+  for (int j = 0; j <= nt; ++j) { sf[j] = std::sin(h.th0 + j * dth); cf[j] = std::cos(h.th0 + j * dth); }
   std::vector<double> tab;
-  for (int i = 0; i < h.nr; ++i) tab.push_back(R1 + (i + 0.5) * h.dr);
-  for (int i = 0; i <= h.nr; ++i) tab.push_back(R1 + i * h.dr);
-  for (int j = 0; j < h.nt; ++j) tab.push_back(std::sin(h.th0 + (j + 0.5) * h.dth));
-  for (int j = 0; j <= h.nt; ++j) tab.push_back(std::sin(h.th0 + j * h.dth));
-  for (int j = 0; j < h.nt; ++j) tab.push_back(std::cos(h.th0 + (j + 0.5) * h.dth));
-  for (int j = 0; j <= h.nt; ++j) tab.push_back(std::cos(h.th0 + j * h.dth));
+  std::vector<std::pair<const double**, size_t>> slots;   // (Geo member, offset)
+  auto put = [&](const double** member, const std::vector<double>& v) {
+    slots.push_back({member, tab.size()});
+    tab.insert(tab.end(), v.begin(), v.end());
+  };
+  auto vec = [](int n, auto f) { std::vector<double> v(n); for (int q = 0; q < n; ++q) v[q] = f(q); return v; };
+  const double dr2 = dr * dr, dt2 = dth * dth;
+  put(&g.rc, rc); put(&g.rf, rf); put(&g.sc, sc); put(&g.sf, sf); put(&g.cc, cc); put(&g.cf, cf);
+  // r at centres
+  put(&g.ir_c, vec(nr, [&](int i) { return 1.0 / rc[i]; }));
+  put(&g.ir2_c, vec(nr, [&](int i) { return 1.0 / (rc[i] * rc[i]); }));
+  put(&g.lr_cm, vec(nr, [&](int i) { return rf[i] * rf[i] / (rc[i] * rc[i] * dr2); }));
+  put(&g.lr_cp, vec(nr, [&](int i) { return rf[i + 1] * rf[i + 1] / (rc[i] * rc[i] * dr2); }));
+  put(&g.idv1_c, vec(nr, [&](int i) { return 1.0 / (rc[i] * rc[i] * dr); }));
+  // r on faces (entries at the walls i = 0, nr are never used by solved rows)
+  auto rcs = [&](int i) { return rc[std::min(std::max(i, 0), nr - 1)]; };
+  auto rfs = [&](int i) { return rf[std::min(std::max(i, 0), nr)]; };
+  put(&g.ir_f, vec(nr + 1, [&](int i) { return 1.0 / rf[i]; }));
+  put(&g.ir2_f, vec(nr + 1, [&](int i) { return 1.0 / (rf[i] * rf[i]); }));
+  put(&g.lr_fm, vec(nr + 1, [&](int i) { return rcs(i - 1) * rcs(i - 1) / (rf[i] * rf[i] * dr2); }));
+  put(&g.lr_fp, vec(nr + 1, [&](int i) { return rcs(i) * rcs(i) / (rf[i] * rf[i] * dr2); }));
+  put(&g.mr_m, vec(nr + 1, [&](int i) { return rfs(i - 1) * rfs(i - 1) / (rf[i] * rf[i] * rf[i] * dr); }));
+  put(&g.mr_p, vec(nr + 1, [&](int i) { return rfs(i + 1) * rfs(i + 1) / (rf[i] * rf[i] * rf[i] * dr); }));
+  put(&g.d11_m, vec(nr + 1, [&](int i) { return rfs(i - 1) * rfs(i - 1) / (rcs(i - 1) * rcs(i - 1) * dr2); }));
+  put(&g.d11_p, vec(nr + 1, [&](int i) { return rfs(i + 1) * rfs(i + 1) / (rcs(i) * rcs(i) * dr2); }));
+  put(&g.d11_0, vec(nr + 1, [&](int i) {
+    return rf[i] * rf[i] * (1.0 / (rcs(i) * rcs(i)) + 1.0 / (rcs(i - 1) * rcs(i - 1))) / dr2; }));
+  put(&g.rf2, vec(nr + 1, [&](int i) { return rf[i] * rf[i]; }));
+  // theta at centres
+  put(&g.is_c, vec(nt, [&](int j) { return 1.0 / sc[j]; }));
+  put(&g.is2_c, vec(nt, [&](int j) { return 1.0 / (sc[j] * sc[j]); }));
+  put(&g.cot_c, vec(nt, [&](int j) { return cc[j] / sc[j]; }));
+  put(&g.lt_cm, vec(nt, [&](int j) { return sf[j] / (sc[j] * dt2); }));
+  put(&g.lt_cp, vec(nt, [&](int j) { return sf[j + 1] / (sc[j] * dt2); }));
+  // theta on faces (entries j = 0, nt unused by solved rows)
+  auto scs = [&](int j) { return sc[std::min(std::max(j, 0), nt - 1)]; };
+  auto sfs = [&](int j) { return sf[std::min(std::max(j, 0), nt)]; };
+  put(&g.is_f, vec(nt + 1, [&](int j) { return 1.0 / sf[j]; }));
+  put(&g.is2_f, vec(nt + 1, [&](int j) { return 1.0 / (sf[j] * sf[j]); }));
+  put(&g.cot_f, vec(nt + 1, [&](int j) { return cf[j] / sf[j]; }));
+  put(&g.lt_fm, vec(nt + 1, [&](int j) { return scs(j - 1) / (sf[j] * dt2); }));
+  put(&g.lt_fp, vec(nt + 1, [&](int j) { return scs(j) / (sf[j] * dt2); }));
+  put(&g.mt_m, vec(nt + 1, [&](int j) { return cf[j] * sfs(j - 1) / (sf[j] * sf[j] * dth); }));
+  put(&g.mt_p, vec(nt + 1, [&](int j) { return cf[j] * sfs(j + 1) / (sf[j] * sf[j] * dth); }));
+  put(&g.d22_m, vec(nt + 1, [&](int j) { return sfs(j - 1) / (scs(j - 1) * dt2); }));
+  put(&g.d22_p, vec(nt + 1, [&](int j) { return sfs(j + 1) / (scs(j) * dt2); }));
+  put(&g.d22_0, vec(nt + 1, [&](int j) { return sf[j] * (1.0 / scs(j) + 1.0 / scs(j - 1)) / dt2; }));
+  g.idr = 1.0 / dr; g.idth = 1.0 / dth; g.idph = 1.0 / h.dph; g.idph2 = g.idph * g.idph;
+  g.iR1sq = 1.0 / (R1 * R1);
   yy_status s;
   const double* dtab = nullptr;
   if ((s = upload(ctx, tab, &dtab)) != YY_OK) { yy_destroy(ctx); return s; }
-  g.rc = dtab;
-  g.rf = g.rc + h.nr;
-  g.sc = g.rf + h.nr + 1;
-  g.sf = g.sc + h.nt;
-  g.cc = g.sf + h.nt + 1;
-  g.cf = g.cc + h.nt;
+  for (auto& sl : slots) *sl.first = dtab + sl.second;
   if ((s = build_tables(ctx, h)) != YY_OK) { std::fprintf(stderr, "yy_create: %s\n", ctx->err.c_str()); yy_destroy(ctx); return s; }
   // fields
   long long maxk = 0;

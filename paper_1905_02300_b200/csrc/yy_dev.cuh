@@ -31,7 +31,26 @@ struct Geo {
   const double* sf;               // sin(theta faces)   [nt+1]
   const double* cc;               // cos(theta centres) [nt]
   const double* cf;               // cos(theta faces)   [nt+1]
+  // reciprocals of the uniform spacings and the hat constant 1/R1^2
+  double idr, idth, idph, idph2, iR1sq;
+  // 1-D factor tables (host fp64): every row weight is a product of these,
+  // so no kernel divides.  _c: nodes at cell centres, _f: nodes on faces.
+  const double *ir_c, *ir2_c, *lr_cm, *lr_cp, *idv1_c;                  // [nr]
+  const double *ir_f, *ir2_f, *lr_fm, *lr_fp, *mr_m, *mr_p, *d11_m, *d11_p, *d11_0, *rf2;   // [nr+1]
+  const double *is_c, *is2_c, *cot_c, *lt_cm, *lt_cp;                    // [nt]
+  const double *is_f, *is2_f, *cot_f, *lt_fm, *lt_fp, *mt_m, *mt_p, *d22_m, *d22_p, *d22_0;  // [nt+1]
 };
+
+// 1/x to full fp64 precision (<= 1 ulp): hardware approximation refined by two
+// Newton steps.  Used for the Thomas / PCR pivots.
+__device__ __forceinline__ double frcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
 
 __host__ __device__ __forceinline__ int NRk(const Geo& g, int K) { return g.nr + (K == KR); }
 __host__ __device__ __forceinline__ int NTk(const Geo& g, int K) { return g.nt + (K == KT); }
@@ -90,99 +109,94 @@ __device__ __forceinline__ double abar_p(const Geo& g, const Astar& A, int i, in
                  __ldg(a + IX<KP>(g, i, j, k)) + __ldg(a + IX<KP>(g, i, j, k + 1)));
 }
 
-// Node coordinates of kind K.
+// Node coordinates and 1-D factors at the nodes of kind K.
 template <int K> __device__ __forceinline__ double rnode(const Geo& g, int i) {
   return K == KR ? __ldg(g.rf + i) : __ldg(g.rc + i);
 }
 template <int K> __device__ __forceinline__ double snode(const Geo& g, int j) {
   return K == KT ? __ldg(g.sf + j) : __ldg(g.sc + j);
 }
-template <int K> __device__ __forceinline__ double cnode(const Geo& g, int j) {
-  return K == KT ? __ldg(g.cf + j) : __ldg(g.cc + j);
+template <int K> __device__ __forceinline__ double irn(const Geo& g, int i) {    // 1/r
+  return K == KR ? __ldg(g.ir_f + i) : __ldg(g.ir_c + i);
+}
+template <int K> __device__ __forceinline__ double ir2n(const Geo& g, int i) {   // 1/r^2
+  return K == KR ? __ldg(g.ir2_f + i) : __ldg(g.ir2_c + i);
+}
+template <int K> __device__ __forceinline__ double isn(const Geo& g, int j) {    // 1/sin(theta)
+  return K == KT ? __ldg(g.is_f + j) : __ldg(g.is_c + j);
+}
+template <int K> __device__ __forceinline__ double is2n(const Geo& g, int j) {   // 1/sin^2(theta)
+  return K == KT ? __ldg(g.is2_f + j) : __ldg(g.is2_c + j);
+}
+template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {   // cot(theta)
+  return K == KT ? __ldg(g.cot_f + j) : __ldg(g.cot_c + j);
 }
 
 // Row weights (am, a0, ap) of the directional operator L_{Q,AX} at node (i,j,k):
 //   (L X)_n = am X_{n-e} + a0 X_n + ap X_{n+e}.
 // HAT selects the implicit (split) operator with Delta^_thth, Delta^_phph
 // versus the full Delta_thth, Delta_phph of the explicit L psi^*.
+// Weights are products of the 1-D tables of Geo (see yy_api.cu: host_tables).
 template <int Q, int AX, bool HAT>
 __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j, int k,
                                      double& am, double& a0, double& ap) {
   constexpr int K = kind_of(Q);
   const double D = (Q == QT) ? g.kap : g.nu;
-  const double rn = rnode<K>(g, i);
   if (AX == 0) {
     // Delta_rr = (1/r^2) d_r(r^2 d_r), flux form; - a_r d_r
-    double rm, rp;
-    if (K == KR) { rm = __ldg(g.rc + i - 1); rp = __ldg(g.rc + i); }
-    else { rm = __ldg(g.rf + i); rp = __ldg(g.rf + i + 1); }
-    const double inv = 1.0 / (rn * rn * g.dr * g.dr);
-    const double dm = D * rm * rm * inv, dp = D * rp * rp * inv;
-    const double adv = abar_r<K>(g, A, i, j, k) * (0.5 / g.dr);
+    const double dm = D * (K == KR ? __ldg(g.lr_fm + i) : __ldg(g.lr_cm + i));
+    const double dp = D * (K == KR ? __ldg(g.lr_fp + i) : __ldg(g.lr_cp + i));
+    const double adv = abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
     if (Q == QUR) {
       // nu(-2u/r^2 + (2/r^3) d_r(r^2 u)) (eq:r_comp L393) + c_chi D11 (RD11)
-      const double fm = __ldg(g.rf + i - 1), fp = __ldg(g.rf + i + 1);
-      const double cm = __ldg(g.rc + i - 1), cp = __ldg(g.rc + i);
-      const double r3 = rn * rn * rn;
-      a0 -= 2.0 * g.nu / (rn * rn);
-      ap += g.nu * fp * fp / (r3 * g.dr);
-      am -= g.nu * fm * fm / (r3 * g.dr);
-      const double idr2 = 1.0 / (g.dr * g.dr);
-      ap += g.cchi * fp * fp / (cp * cp) * idr2;
-      am += g.cchi * fm * fm / (cm * cm) * idr2;
-      a0 -= g.cchi * rn * rn * (1.0 / (cp * cp) + 1.0 / (cm * cm)) * idr2;
+      a0 -= 2.0 * g.nu * __ldg(g.ir2_f + i);
+      ap += g.nu * __ldg(g.mr_p + i);
+      am -= g.nu * __ldg(g.mr_m + i);
+      ap += g.cchi * __ldg(g.d11_p + i);
+      am += g.cchi * __ldg(g.d11_m + i);
+      a0 -= g.cchi * __ldg(g.d11_0 + i);
     }
   } else if (AX == 1) {
     // Delta_thth = (1/(rho^2 sin th)) d_th(sin th d_th), rho = R1 (hat) or r; - (a_th/r) d_th
-    const double sn = snode<K>(g, j);
-    double sm, sp;
-    if (K == KT) { sm = __ldg(g.sc + j - 1); sp = __ldg(g.sc + j); }
-    else { sm = __ldg(g.sf + j); sp = __ldg(g.sf + j + 1); }
-    const double rho2 = HAT ? g.R1 * g.R1 : rn * rn;
-    const double inv = D / (rho2 * sn * g.dth * g.dth);
-    const double dm = sm * inv, dp = sp * inv;
-    const double adv = abar_t<K>(g, A, i, j, k) * (0.5 / (rn * g.dth));
+    const double rho = HAT ? g.iR1sq : ir2n<K>(g, i);
+    const double dm = D * rho * (K == KT ? __ldg(g.lt_fm + j) : __ldg(g.lt_cm + j));
+    const double dp = D * rho * (K == KT ? __ldg(g.lt_fp + j) : __ldg(g.lt_cp + j));
+    const double adv = abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
     if (Q == QUT) {
       // nu(-u/(r^2 sin^2) + (2cos/(r^2 sin^2)) d_th(u sin)) (RD13) + c_chi D22 (RD11)
       // - (a_r/r) u (RD14)
-      const double cn = cnode<K>(g, j);
-      const double r2 = rn * rn;
-      const double sfm = __ldg(g.sf + j - 1), sfp = __ldg(g.sf + j + 1);
-      const double scm = __ldg(g.sc + j - 1), scp = __ldg(g.sc + j);
-      a0 -= g.nu / (r2 * sn * sn);
-      const double kk = g.nu * cn / (r2 * sn * sn * g.dth);
-      ap += kk * sfp;
-      am -= kk * sfm;
-      const double idt2 = 1.0 / (r2 * g.dth * g.dth);
-      ap += g.cchi * sfp / scp * idt2;
-      am += g.cchi * sfm / scm * idt2;
-      a0 -= g.cchi * sn * (1.0 / scp + 1.0 / scm) * idt2;
-      a0 -= abar_r<K>(g, A, i, j, k) / rn;
+      const double ir2 = __ldg(g.ir2_c + i);
+      a0 -= g.nu * ir2 * __ldg(g.is2_f + j);
+      ap += g.nu * ir2 * __ldg(g.mt_p + j);
+      am -= g.nu * ir2 * __ldg(g.mt_m + j);
+      ap += g.cchi * ir2 * __ldg(g.d22_p + j);
+      am += g.cchi * ir2 * __ldg(g.d22_m + j);
+      a0 -= g.cchi * ir2 * __ldg(g.d22_0 + j);
+      a0 -= abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
     }
   } else {
     // Delta_phph = d_phph/(r^2 sin^2 th); hat: 1/(R1^2 sin^2 th_1); - (a_ph/(r sin th)) d_ph
-    const double sn = snode<K>(g, j);
-    const double c = HAT ? D * g.hatph : D / (rn * rn * sn * sn * g.dph * g.dph);
-    const double adv = abar_p<K>(g, A, i, j, k) * (0.5 / (rn * sn * g.dph));
+    const double ir = irn<K>(g, i), is = isn<K>(g, j);
+    const double c = HAT ? D * g.hatph : D * ir2n<K>(g, i) * is2n<K>(g, j) * g.idph2;
+    const double adv = abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is;
     am = c + adv;
     ap = c - adv;
     a0 = -2.0 * c;
     if (Q == QUP) {
       // nu(-u/(r^2 sin^2)) + c_chi D33 (RD12) - ((a_r + a_th cot)/r) u
-      const double cn = cnode<K>(g, j);
-      const double r2s2 = rn * rn * sn * sn;
-      a0 -= g.nu / r2s2;
-      const double c2 = g.cchi / (r2s2 * g.dph * g.dph);
+      const double r2s2 = __ldg(g.ir2_c + i) * __ldg(g.is2_c + j);
+      a0 -= g.nu * r2s2;
+      const double c2 = g.cchi * r2s2 * g.idph2;
       am += c2;
       ap += c2;
       a0 -= 2.0 * c2;
-      a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * cn / sn) / rn;
+      a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
     }
   }
 }

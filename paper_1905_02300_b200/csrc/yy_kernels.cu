@@ -76,15 +76,15 @@ __device__ __forceinline__ bool solved(const Geo& g, int i, int j, int k) {
 
 // divergence contributions at cell centre (i,j,k) of one patch
 __device__ __forceinline__ double div1(const Geo& g, const double* ur, int i, int j, int k) {
-  const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1), c = __ldg(g.rc + i);
-  return (f1 * f1 * ur[IX<KR>(g, i + 1, j, k)] - f0 * f0 * ur[IX<KR>(g, i, j, k)]) / (c * c * g.dr);
+  return (__ldg(g.rf2 + i + 1) * ur[IX<KR>(g, i + 1, j, k)] - __ldg(g.rf2 + i) * ur[IX<KR>(g, i, j, k)]) *
+         __ldg(g.idv1_c + i);
 }
 __device__ __forceinline__ double div2(const Geo& g, const double* ut, int i, int j, int k) {
-  return (__ldg(g.sf + j + 1) * ut[IX<KT>(g, i, j + 1, k)] - __ldg(g.sf + j) * ut[IX<KT>(g, i, j, k)]) /
-         (__ldg(g.rc + i) * __ldg(g.sc + j) * g.dth);
+  return (__ldg(g.sf + j + 1) * ut[IX<KT>(g, i, j + 1, k)] - __ldg(g.sf + j) * ut[IX<KT>(g, i, j, k)]) *
+         (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idth);
 }
 __device__ __forceinline__ double div3(const Geo& g, const double* up, int i, int j, int k) {
-  return (up[IX<KP>(g, i, j, k + 1)] - up[IX<KP>(g, i, j, k)]) / (__ldg(g.rc + i) * __ldg(g.sc + j) * g.dph);
+  return (up[IX<KP>(g, i, j, k + 1)] - up[IX<KP>(g, i, j, k)]) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
 }
 
 __device__ __forceinline__ double omega(const Geo& g, double r, double s) {
@@ -160,10 +160,10 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
           const double d3 = 1.5 * div3(g, upn, ii, j, k) - 0.5 * div3(g, upm, ii, j, k);
           return d2 + d3;
         };
-        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i - 1, j, k)]) / g.dr;
-        E += g.cchi * (dd(i) - dd(i - 1)) / g.dr;
+        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i - 1, j, k)]) * g.idr;
+        E += g.cchi * (dd(i) - dd(i - 1)) * g.idr;
         const double at_ = abar_t<KR>(g, A, i, j, k), ap_ = abar_p<KR>(g, A, i, j, k);
-        E += (at_ * at_ + ap_ * ap_) / rn;
+        E += (at_ * at_ + ap_ * ap_) * __ldg(g.ir_f + i);
         (void)uts;
       } else if (Q == QUT) {
         // -(1/r) d_th p^n + c_chi (1/r) d_th(div3 u_ph^*) + a_ph^2 cot(th)/r   (eq:theta_comp, RD14)
@@ -171,13 +171,14 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
         const double *upn = a.upn[s] + op, *upm = a.upm[s] + op;
         const double d3 = 1.5 * div3(g, upn, i, j, k) - 0.5 * div3(g, upm, i, j, k);
         const double d3m = 1.5 * div3(g, upn, i, j - 1, k) - 0.5 * div3(g, upm, i, j - 1, k);
-        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i, j - 1, k)]) / (rn * g.dth);
-        E += g.cchi * (d3 - d3m) / (rn * g.dth);
+        const double irdt = __ldg(g.ir_c + i) * g.idth;
+        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i, j - 1, k)]) * irdt;
+        E += g.cchi * (d3 - d3m) * irdt;
         const double ap_ = abar_p<KT>(g, A, i, j, k);
-        E += ap_ * ap_ * __ldg(g.cf + j) / (__ldg(g.sf + j) * rn);
+        E += ap_ * ap_ * __ldg(g.cot_f + j) * __ldg(g.ir_c + i);
       } else {
         // -(1/(r sin th)) d_ph p^n   (eq:phi_comp)
-        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i, j, k - 1)]) / (rn * __ldg(g.sc + j) * g.dph);
+        E += -(p[IX<KC>(g, i, j, k)] - p[IX<KC>(g, i, j, k - 1)]) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
       }
     }
     const double Lf = applyL<Q, false>(g, A, i, j, k, S);
@@ -223,14 +224,13 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
       const long long q = IX<KR>(g, ii, jj, k);
       return 0.5 * (uri[q] + urn[q]);
     };
-    auto d1 = [&](int jj) {
-      const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1), c = __ldg(g.rc + i);
-      return (f1 * f1 * ub(i + 1, jj) - f0 * f0 * ub(i, jj)) / (c * c * g.dr);
-    };
+    const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
+    auto d1 = [&](int jj) { return (f1 * ub(i + 1, jj) - f0 * ub(i, jj)) * iv; };
+    const double ir = __ldg(g.ir_c + i);
     const double d1a = d1(j - 1), d1b = d1(j);
-    E = g.cchi * (d1b - d1a) / (rn * g.dth);
-    E += g.nu * (2.0 / (rn * rn)) * 0.5 * ((ub(i, j) - ub(i, j - 1)) + (ub(i + 1, j) - ub(i + 1, j - 1))) / g.dth;
-    E += g.nu * (2.0 * __ldg(g.cf + j) / (__ldg(g.sf + j) * rn)) * 0.5 * (d1a + d1b);
+    E = g.cchi * (d1b - d1a) * (ir * g.idth);
+    E += g.nu * (2.0 * ir * ir) * 0.5 * ((ub(i, j) - ub(i, j - 1)) + (ub(i + 1, j) - ub(i + 1, j - 1))) * g.idth;
+    E += g.nu * (2.0 * __ldg(g.cot_f + j) * ir) * 0.5 * (d1a + d1b);
   } else if (Q == QUP) {
     // c_chi (D31 ub_r + D32 ub_th) + nu((2/(r^2 sin)) d_ph ub_r + (2cos/(r^2 sin^2)) d_ph ub_th)
     const long long orr = patch * psize(g, KR), ot = patch * psize(g, KT);
@@ -243,17 +243,19 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
       const long long q = IX<KT>(g, i, jj, kk);
       return 0.5 * (uti[q] + utn[q]);
     };
-    const double sn = __ldg(g.sc + j), cn = __ldg(g.cc + j);
-    const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1);
+    const double ir = __ldg(g.ir_c + i), is = __ldg(g.is_c + j), ct = __ldg(g.cot_c + j);
+    const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
     const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1);
+    const double rsdt = ir * is * g.idth;
     auto e = [&](int kk) {
-      const double dd1 = (f1 * f1 * ubr(i + 1, kk) - f0 * f0 * ubr(i, kk)) / (rn * rn * g.dr);
-      const double dd2 = (s1 * ubt(j + 1, kk) - s0 * ubt(j, kk)) / (rn * sn * g.dth);
+      const double dd1 = (f1 * ubr(i + 1, kk) - f0 * ubr(i, kk)) * iv;
+      const double dd2 = (s1 * ubt(j + 1, kk) - s0 * ubt(j, kk)) * rsdt;
       return dd1 + dd2;
     };
-    E = g.cchi * (e(k) - e(k - 1)) / (rn * sn * g.dph);
-    E += g.nu * (2.0 / (rn * rn * sn)) * 0.5 * ((ubr(i, k) - ubr(i, k - 1)) + (ubr(i + 1, k) - ubr(i + 1, k - 1))) / g.dph;
-    E += g.nu * (2.0 * cn / (rn * rn * sn * sn)) * 0.5 * ((ubt(j, k) - ubt(j, k - 1)) + (ubt(j + 1, k) - ubt(j + 1, k - 1))) / g.dph;
+    const double rsdp = ir * is * g.idph;
+    E = g.cchi * (e(k) - e(k - 1)) * rsdp;
+    E += g.nu * (2.0 * ir * rsdp) * 0.5 * ((ubr(i, k) - ubr(i, k - 1)) + (ubr(i + 1, k) - ubr(i + 1, k - 1)));
+    E += g.nu * (2.0 * ct * ir * rsdp) * 0.5 * ((ubt(j, k) - ubt(j, k - 1)) + (ubt(j + 1, k) - ubt(j + 1, k - 1)));
   }
   if (S == 2 && Q != QT) {
     // -1/2 grad(p1^(k) - p1^n)   (RD18)
@@ -262,9 +264,9 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
       const long long q = IX<KC>(g, ii, jj, kk);
       return pi_[q] - pn[q];
     };
-    if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) / g.dr;
-    if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) / (rn * g.dth);
-    if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) / (rn * __ldg(g.sc + j) * g.dph);
+    if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) * g.idr;
+    if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) * (__ldg(g.ir_c + i) * g.idth);
+    if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
   }
   const double LX = applyL<Q, true>(g, A, i, j, k, X);
   a.R[po + node] = a.G[po + node] + g.tau * E - (X.c - 0.5 * g.tau * LX);
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
       }
       const double lo = (m == 0) ? 0.0 : -th * am;
       const double up = -th * ap;
-      const double inv = 1.0 / (di - lo * cprev);
+      const double inv = frcp(di - lo * cprev);
       const long long q = base + m * stride;
       const double cp = up * inv;
       const double dp = (R[q] - lo * dprev) * inv;
@@ -352,6 +354,103 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
+// K3: phi-line sweep (the contiguous axis).  One warp per line: the line's rows
+// are built with coalesced loads (lane = consecutive k) into shared memory,
+// normalised (b = 1), reduced by 5 steps of parallel cyclic reduction
+// (stride 1..16) into 32 independent interleaved systems (k = l mod 32), each
+// solved by one lane with Thomas; coalesced write-back.  Same rows, same end
+// conditions and same result (up to rounding) as the serial Thomas of k_sweep.
+// smem per warp: 2 buffers x (a, c, d) x n doubles.
+// ---------------------------------------------------------------------------------
+template <int Q, bool FINAL>
+__global__ void __launch_bounds__(128) k_sweep_phi(Geo g, SweepArgs a, int nwarps) {
+  constexpr int K = kind_of(Q);
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int patch = blockIdx.y;
+  const int n = NPk(g, K) - 2;                       // unknowns k = 1..NP-2
+  const int nj = NTk(g, K) - 2;
+  const int ni = (K == KR) ? g.nr - 1 : g.nr;
+  const long long L = (long long)blockIdx.x * nwarps + warp;
+  double wsum = 0.0;
+  if (warp < nwarps && L < (long long)ni * nj) {
+    const int i = i_lo<K>() + (int)(L / nj), j = 1 + (int)(L % nj);
+    double* A0 = sm + (size_t)warp * 6 * n;
+    double* C0 = A0 + n;
+    double* D0 = C0 + n;
+    double* A1 = D0 + n;
+    double* C1 = A1 + n;
+    double* D1 = C1 + n;
+    const long long po = patch * psize(g, K);
+    Astar As{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+    double* __restrict__ R = a.R + po;
+    const long long base = IX<K>(g, i, j, 1);
+    const double th = 0.5 * g.tau;
+    for (int m = lane; m < n; m += 32) {
+      double am, a0, ap;
+      coef<Q, 2, true>(g, As, i, j, 1 + m, am, a0, ap);
+      const double inv = frcp(1.0 - th * a0);
+      A0[m] = (m == 0) ? 0.0 : -th * am * inv;
+      C0[m] = (m == n - 1) ? 0.0 : -th * ap * inv;
+      D0[m] = R[base + m] * inv;
+    }
+    __syncwarp();
+    double *Ai = A0, *Ci = C0, *Di = D0, *Ao = A1, *Co = C1, *Do = D1;
+#pragma unroll 1
+    for (int s = 1; s < 32; s <<= 1) {
+      for (int m = lane; m < n; m += 32) {
+        const double am_ = Ai[m], cm_ = Ci[m];
+        double al = 0.0, cl = 0.0, dl = 0.0, ar_ = 0.0, cr = 0.0, dr = 0.0;
+        if (m - s >= 0) { al = Ai[m - s]; cl = Ci[m - s]; dl = Di[m - s]; }
+        if (m + s < n) { ar_ = Ai[m + s]; cr = Ci[m + s]; dr = Di[m + s]; }
+        const double inv = frcp(1.0 - am_ * cl - cm_ * ar_);
+        Ao[m] = -am_ * al * inv;
+        Co[m] = -cm_ * cr * inv;
+        Do[m] = (Di[m] - am_ * dl - cm_ * dr) * inv;
+      }
+      __syncwarp();
+      double* t;
+      t = Ai; Ai = Ao; Ao = t;
+      t = Ci; Ci = Co; Co = t;
+      t = Di; Di = Do; Do = t;
+    }
+    // 32 independent systems: rows m = lane + 32 t couple m -/+ 32
+    double cp = 0.0, dp = 0.0;
+    for (int m = lane; m < n; m += 32) {
+      const double inv = frcp(1.0 - Ai[m] * cp);
+      cp = Ci[m] * inv;
+      dp = (Di[m] - Ai[m] * dp) * inv;
+      Ci[m] = cp;
+      Di[m] = dp;
+    }
+    const int last = lane + 32 * ((n - 1 - lane) / 32);
+    double x = 0.0;
+    if (lane < n) {
+      for (int m = last; m >= 0; m -= 32) {
+        x = (m == last) ? Di[m] : Di[m] - Ci[m] * x;
+        Di[m] = x;
+      }
+    }
+    __syncwarp();
+    if (FINAL) {
+      double* __restrict__ psi = a.psi + po;
+      const double w0 = omega(g, rnode<K>(g, i), snode<K>(g, j));
+      for (int m = lane; m < n; m += 32) {
+        const double v = Di[m];
+        psi[base + m] += v;
+        wsum += w0 * v * v;
+      }
+    } else {
+      for (int m = lane; m < n; m += 32) R[base + m] = Di[m];
+    }
+  }
+  if (FINAL) {
+    const double t = block_sum<128>(wsum);
+    if (threadIdx.x == 0) a.part[(long long)patch * a.maxb + blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // K7: pressure updates (eq:nst_Mass1 P:L457; system 2 per RD18)
 // ---------------------------------------------------------------------------------
 template <int S>
@@ -368,16 +467,17 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
     const double *uti = a.utit + ot, *utn = a.utn + ot;
     const double *upi = a.upit + op, *upn = a.upn + op;
     const double rn = __ldg(g.rc + i), sn = __ldg(g.sc + j);
-    const double f0 = __ldg(g.rf + i), f1 = __ldg(g.rf + i + 1);
+    const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1);
     const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1);
+    const double rs = __ldg(g.ir_c + i) * __ldg(g.is_c + j);
     const double ur0 = 0.5 * (uri[IX<KR>(g, i, j, k)] + urn[IX<KR>(g, i, j, k)]);
     const double ur1 = 0.5 * (uri[IX<KR>(g, i + 1, j, k)] + urn[IX<KR>(g, i + 1, j, k)]);
     const double ut0 = 0.5 * (uti[IX<KT>(g, i, j, k)] + utn[IX<KT>(g, i, j, k)]);
     const double ut1 = 0.5 * (uti[IX<KT>(g, i, j + 1, k)] + utn[IX<KT>(g, i, j + 1, k)]);
     const double up0 = 0.5 * (upi[IX<KP>(g, i, j, k)] + upn[IX<KP>(g, i, j, k)]);
     const double up1 = 0.5 * (upi[IX<KP>(g, i, j, k + 1)] + upn[IX<KP>(g, i, j, k + 1)]);
-    const double dv = (f1 * f1 * ur1 - f0 * f0 * ur0) / (rn * rn * g.dr) +
-                      (s1 * ut1 - s0 * ut0) / (rn * sn * g.dth) + (up1 - up0) / (rn * sn * g.dph);
+    const double dv = (f1 * ur1 - f0 * ur0) * __ldg(g.idv1_c + i) + (s1 * ut1 - s0 * ut0) * (rs * g.idth) +
+                      (up1 - up0) * (rs * g.idph);
     const long long q = pc + IX<KC>(g, i, j, k);
     double nv;
     if (S == 1) nv = a.pn[q] - g.inv_chi * dv;
@@ -516,9 +616,29 @@ void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t s
   else { if (s == 1) k_resid<QUP, 1><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); else k_resid<QUP, 2><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); }
 }
 
+template <int Q, bool F>
+static int sweep_phi(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  const int n = NPk(g, K) - 2;
+  const size_t per_warp = (size_t)6 * n * sizeof(double);
+  int nw = (int)((200 * 1024) / per_warp);   // <= 227 KB opt-in per block on sm_100
+  nw = nw < 1 ? 1 : (nw > 4 ? 4 : nw);
+  const long long lines = (long long)((K == KR) ? g.nr - 1 : g.nr) * (NTk(g, K) - 2);
+  const int blocks = (int)((lines + nw - 1) / nw);
+  const size_t smem = per_warp * nw;
+  static size_t attr_set = 0;
+  if (smem > 48 * 1024 && smem > attr_set) {
+    cudaFuncSetAttribute(k_sweep_phi<Q, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = smem;
+  }
+  k_sweep_phi<Q, F><<<dim3(blocks, npatch), 128, smem, st>>>(g, a, nw);
+  return blocks;
+}
+
 template <int Q, int AX, bool F>
 static int sweep_one(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
+  if (AX == 2) return sweep_phi<Q, F>(g, a, npatch, st);
   dim3 grid;
   if (AX == 0) grid = dim3((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, npatch);
   else if (AX == 1) grid = dim3((NPk(g, K) - 2 + 127) / 128, (K == KR ? g.nr - 1 : g.nr), npatch);
