@@ -482,7 +482,7 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
       ra.nblk[base + 3] = launch_pres(g, s, pa, st);
     }
     {
-      ProfScope ps(ctx, "reduce", 1);
+      ProfScope ps(ctx, "reduce", 2);
       launch_reduce(ctx->part, ra, ctx->red, st);          // O10
     }
     CK(cudaGetLastError());

@@ -91,7 +91,8 @@ __device__ __forceinline__ double omega(const Geo& g, double r, double s) {
   return r * r * s * g.dr * g.dth * g.dph;
 }
 
-// deterministic block sum (fixed thread -> data assignment, fixed tree)
+// deterministic block sum (fixed thread -> data assignment, fixed tree);
+// blockDim.x <= NT_, multiple of 32
 template <int NT_>
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double sh[NT_ / 32];
@@ -101,7 +102,7 @@ __device__ __forceinline__ double block_sum(double v) {
   __syncthreads();
   double t = 0.0;
   if (threadIdx.x == 0)
-    for (int q = 0; q < NT_ / 32; ++q) t += sh[q];
+    for (int q = 0; q < (int)(blockDim.x / 32); ++q) t += sh[q];
   return t;   // valid in thread 0
 }
 
@@ -279,8 +280,9 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
 // In place on R (d' then x); c' in scratch C.  FINAL: psi += x and norm partial.
 // Line grid: AX=0: x -> k, y -> j;  AX=1: x -> k, y -> i;  AX=2: x -> j, y -> i.  z -> patch.
 // ---------------------------------------------------------------------------------
-template <int Q, int AX, bool FINAL>
+template <int Q, int AX, bool FINAL, bool SMC>
 __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
+  extern __shared__ double csm[];   // SMC: c' column of this thread at csm[m * blockDim.x + threadIdx.x]
   constexpr int K = kind_of(Q);
   const int patch = blockIdx.z;
   int i = 0, j = 0, k = 0, n = 0;
@@ -310,39 +312,76 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
     double* __restrict__ R = a.R + po;
     double* __restrict__ C = a.C + po;
     const long long base = IX<K>(g, i, j, k);
+    auto cidx = [&](int m) -> long long {
+      return SMC ? (long long)m * blockDim.x + threadIdx.x : base + m * stride;
+    };
+    double* __restrict__ Cs = SMC ? csm : C;
     const double th = 0.5 * g.tau;
     double cprev = 0.0, dprev = 0.0;
-    for (int m = 0; m < n; ++m) {
-      const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j, kk = (AX == 2) ? k + m : k;
-      double am, a0, ap;
-      coef<Q, AX, true>(g, A, ii, jj, kk, am, a0, ap);
-      double di = 1.0 - th * a0;
-      if (AX == 0 && K != KR) {
-        if (m == 0) di = 1.0 - th * (a0 - am);
-        if (m == n - 1) di = 1.0 - th * (a0 - ap);
+    // forward elimination, 4 rows per round: the round's loads (rhs and the
+    // read-only a* / table loads inside coef) are all issued before use
+    for (int m0 = 0; m0 < n; m0 += 4) {
+      double rv[4], am[4], a0[4], ap[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) rv[u] = (m0 + u < n) ? R[base + (m0 + u) * stride] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = m0 + u;
+        if (m < n) {
+          const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j, kk = (AX == 2) ? k + m : k;
+          coef<Q, AX, true>(g, A, ii, jj, kk, am[u], a0[u], ap[u]);
+        }
       }
-      const double lo = (m == 0) ? 0.0 : -th * am;
-      const double up = -th * ap;
-      const double inv = frcp(di - lo * cprev);
-      const long long q = base + m * stride;
-      const double cp = up * inv;
-      const double dp = (R[q] - lo * dprev) * inv;
-      C[q] = cp;
-      R[q] = dp;
-      cprev = cp;
-      dprev = dp;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = m0 + u;
+        if (m < n) {
+          double di = 1.0 - th * a0[u];
+          if (AX == 0 && K != KR) {
+            if (m == 0) di = 1.0 - th * (a0[u] - am[u]);
+            if (m == n - 1) di = 1.0 - th * (a0[u] - ap[u]);
+          }
+          const double lo = (m == 0) ? 0.0 : -th * am[u];
+          const double up = -th * ap[u];
+          const double inv = frcp(di - lo * cprev);
+          const long long q = base + m * stride;
+          const double cp = up * inv;
+          const double dp = (rv[u] - lo * dprev) * inv;
+          Cs[cidx(m)] = cp;
+          R[q] = dp;
+          cprev = cp;
+          dprev = dp;
+        }
+      }
     }
     double x = 0.0;
     double* __restrict__ psi = FINAL ? a.psi + po : nullptr;
-    for (int m = n - 1; m >= 0; --m) {
-      const long long q = base + m * stride;
-      x = (m == n - 1) ? R[q] : R[q] - C[q] * x;
-      if (FINAL) {
-        psi[q] += x;
-        const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j;
-        wsum += omega(g, rnode<K>(g, ii), snode<K>(g, jj)) * x * x;
-      } else {
-        R[q] = x;
+    for (int m0 = n - 1; m0 >= 0; m0 -= 4) {
+      double cv[4], dv[4], pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = m0 - u;
+        if (m >= 0) {
+          const long long q = base + m * stride;
+          cv[u] = Cs[cidx(m)];
+          dv[u] = R[q];
+          if (FINAL) pv[u] = psi[q];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = m0 - u;
+        if (m >= 0) {
+          const long long q = base + m * stride;
+          x = (m == n - 1) ? dv[u] : dv[u] - cv[u] * x;
+          if (FINAL) {
+            psi[q] = pv[u] + x;
+            const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j;
+            wsum += omega(g, rnode<K>(g, ii), snode<K>(g, jj)) * x * x;
+          } else {
+            R[q] = x;
+          }
+        }
       }
     }
   }
@@ -354,13 +393,18 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
-// K3: phi-line sweep (the contiguous axis).  One warp per line: the line's rows
-// are built with coalesced loads (lane = consecutive k) into shared memory,
-// normalised (b = 1), reduced by 5 steps of parallel cyclic reduction
-// (stride 1..16) into 32 independent interleaved systems (k = l mod 32), each
-// solved by one lane with Thomas; coalesced write-back.  Same rows, same end
-// conditions and same result (up to rounding) as the serial Thomas of k_sweep.
-// smem per warp: 2 buffers x (a, c, d) x n doubles.
+// K3: phi-line sweep (the contiguous axis), one warp per line, partitioned
+// (Schur-complement) Thomas — the same algebra as the distributed solve of
+// P:L477-480, here across the 32 lanes of a warp:
+//  1. rows built with coalesced loads (lane = consecutive k), stored in shared
+//     memory in chunk layout (lane l owns rows s_l..e_l; element t of every
+//     chunk at smem[t*32 + l]: conflict-free);
+//  2. each lane eliminates its chunk interior s_l..e_l-1 with the chunk ends
+//     as unknowns: x = y + v g_{l-1} + w g_l (g_l = x_{e_l}); one reciprocal per row;
+//  3. row e_l of every chunk gives a tridiagonal system in g_0..g_31, solved by
+//     5 steps of parallel cyclic reduction over warp shuffles;
+//  4. back-fill x, coalesced write-back.
+// Same rows and end conditions as the serial Thomas of k_sweep (x 1e-16 rounding).
 // ---------------------------------------------------------------------------------
 template <int Q, bool FINAL>
 __global__ void __launch_bounds__(128) k_sweep_phi(Geo g, SweepArgs a, int nwarps) {
@@ -371,77 +415,138 @@ __global__ void __launch_bounds__(128) k_sweep_phi(Geo g, SweepArgs a, int nwarp
   const int n = NPk(g, K) - 2;                       // unknowns k = 1..NP-2
   const int nj = NTk(g, K) - 2;
   const int ni = (K == KR) ? g.nr - 1 : g.nr;
+  const int M = (n + 31) >> 5;                       // chunk length: lane l owns rows l*M .. l*M+M-1
+  const int Mp = M | 1;                              // odd pitch: conflict-free chunk-major layout
+  const int nact = (n + M - 1) / M;                  // lanes owning a (possibly shorter last) chunk
+  const float iM = 1.0f / (float)M;
   const long long L = (long long)blockIdx.x * nwarps + warp;
   double wsum = 0.0;
   if (warp < nwarps && L < (long long)ni * nj) {
     const int i = i_lo<K>() + (int)(L / nj), j = 1 + (int)(L % nj);
-    double* A0 = sm + (size_t)warp * 6 * n;
-    double* C0 = A0 + n;
-    double* D0 = C0 + n;
-    double* A1 = D0 + n;
-    double* C1 = A1 + n;
-    double* D1 = C1 + n;
+    // normalised rows x_{e-1} a + x_e + x_{e+1} c = d (b = 1)
+    double* LO = sm + (size_t)warp * 3 * 32 * Mp;
+    double* UP = LO + 32 * Mp;
+    double* RH = UP + 32 * Mp;
     const long long po = patch * psize(g, K);
     Astar As{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
     double* __restrict__ R = a.R + po;
     const long long base = IX<K>(g, i, j, 1);
     const double th = 0.5 * g.tau;
-    for (int m = lane; m < n; m += 32) {
-      double am, a0, ap;
-      coef<Q, 2, true>(g, As, i, j, 1 + m, am, a0, ap);
-      const double inv = frcp(1.0 - th * a0);
-      A0[m] = (m == 0) ? 0.0 : -th * am * inv;
-      C0[m] = (m == n - 1) ? 0.0 : -th * ap * inv;
-      D0[m] = R[base + m] * inv;
+    auto slot = [&](int e) {                         // element -> chunk-major index
+      const int l = (int)(((float)e + 0.5f) * iM);
+      return l * Mp + (e - l * M);
+    };
+    // 1. rows (I - tau/2 A_ph) of this line; 4 elements per lane per round so
+    //    that all of a round's loads are in flight before any is consumed
+    for (int e0 = lane; e0 < n; e0 += 128) {
+      double rv[4], am[4], a0[4], ap[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 32 * u;
+        rv[u] = (e < n) ? R[base + e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 32 * u;
+        if (e < n) coef<Q, 2, true>(g, As, i, j, 1 + e, am[u], a0[u], ap[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 32 * u;
+        if (e < n) {
+          const int q = slot(e);
+          const double inv = frcp(1.0 - th * a0[u]);
+          LO[q] = (e == 0) ? 0.0 : -th * am[u] * inv;
+          UP[q] = (e == n - 1) ? 0.0 : -th * ap[u] * inv;
+          RH[q] = rv[u] * inv;
+        }
+      }
     }
     __syncwarp();
-    double *Ai = A0, *Ci = C0, *Di = D0, *Ao = A1, *Co = C1, *Do = D1;
-#pragma unroll 1
+    // 2. chunk interior elimination (rows t = 0..m-2 of this lane's chunk) with
+    //    x = y + v g_{l-1} + w g_l,  g_l = x at the chunk's last row
+    const int m = (lane < nact) ? min(M, n - lane * M) : 0;
+    const int o = lane * Mp;
+    double cprev = 0.0, yprev = 0.0, vprev = 0.0;
+    for (int t = 0; t + 1 < m; ++t) {
+      const double lo = LO[o + t];
+      const double inv = frcp(1.0 - lo * cprev);
+      const double cp = UP[o + t] * inv;
+      const double yp = (RH[o + t] - lo * yprev) * inv;
+      const double vp = (t ? -lo * vprev : -lo) * inv;
+      UP[o + t] = cp;
+      RH[o + t] = yp;
+      LO[o + t] = vp;
+      cprev = cp; yprev = yp; vprev = vp;
+    }
+    // backward: y, v in place; w (nonzero from the last interior row, w' = -c') kept in UP
+    double Y0 = 0.0, V0 = 0.0, W0 = 1.0;             // x_s as y + v g_{l-1} + w g_l (m = 1: g_l)
+    double Yl = 0.0, Vl = 1.0, Wl = 0.0;             // x_{e-1} (m = 1: g_{l-1})
+    if (m >= 2) {
+      double y = RH[o + m - 2], v = LO[o + m - 2], w = -UP[o + m - 2];
+      UP[o + m - 2] = w;
+      Yl = y; Vl = v; Wl = w;
+      for (int t = m - 3; t >= 0; --t) {
+        const double cp = UP[o + t];
+        y = RH[o + t] - cp * y;
+        v = LO[o + t] - cp * v;
+        w = -cp * w;
+        RH[o + t] = y;
+        LO[o + t] = v;
+        UP[o + t] = w;
+      }
+      Y0 = y; V0 = v; W0 = w;
+    }
+    // 3. reduced tridiagonal system in g (row e_l of every chunk), PCR over shuffles
+    double A = 0.0, B = 1.0, C = 0.0, D = 0.0;
+    {
+      const double Y0n = __shfl_down_sync(0xffffffffu, Y0, 1);
+      const double V0n = __shfl_down_sync(0xffffffffu, V0, 1);
+      const double W0n = __shfl_down_sync(0xffffffffu, W0, 1);
+      if (lane < nact) {
+        const double ae = LO[o + m - 1], ce = UP[o + m - 1];   // row e_l (untouched above)
+        const bool lastl = (lane == nact - 1);
+        A = ae * Vl;
+        B = ae * Wl + 1.0 + (lastl ? 0.0 : ce * V0n);
+        C = lastl ? 0.0 : ce * W0n;
+        D = RH[o + m - 1] - ae * Yl - (lastl ? 0.0 : ce * Y0n);
+      }
+    }
+#pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
-      for (int m = lane; m < n; m += 32) {
-        const double am_ = Ai[m], cm_ = Ci[m];
-        double al = 0.0, cl = 0.0, dl = 0.0, ar_ = 0.0, cr = 0.0, dr = 0.0;
-        if (m - s >= 0) { al = Ai[m - s]; cl = Ci[m - s]; dl = Di[m - s]; }
-        if (m + s < n) { ar_ = Ai[m + s]; cr = Ci[m + s]; dr = Di[m + s]; }
-        const double inv = frcp(1.0 - am_ * cl - cm_ * ar_);
-        Ao[m] = -am_ * al * inv;
-        Co[m] = -cm_ * cr * inv;
-        Do[m] = (Di[m] - am_ * dl - cm_ * dr) * inv;
-      }
-      __syncwarp();
-      double* t;
-      t = Ai; Ai = Ao; Ao = t;
-      t = Ci; Ci = Co; Co = t;
-      t = Di; Di = Do; Do = t;
+      const double Am = __shfl_up_sync(0xffffffffu, A, s), Bm = __shfl_up_sync(0xffffffffu, B, s);
+      const double Cm = __shfl_up_sync(0xffffffffu, C, s), Dm = __shfl_up_sync(0xffffffffu, D, s);
+      const double Ap = __shfl_down_sync(0xffffffffu, A, s), Bp = __shfl_down_sync(0xffffffffu, B, s);
+      const double Cp = __shfl_down_sync(0xffffffffu, C, s), Dp = __shfl_down_sync(0xffffffffu, D, s);
+      const bool hm = lane >= s, hp = lane + s < 32;
+      const double al = hm ? -A * frcp(Bm) : 0.0;
+      const double ga = hp ? -C * frcp(Bp) : 0.0;
+      const double nA = hm ? al * Am : 0.0;
+      const double nC = hp ? ga * Cp : 0.0;
+      B = B + (hm ? al * Cm : 0.0) + (hp ? ga * Ap : 0.0);
+      D = D + (hm ? al * Dm : 0.0) + (hp ? ga * Dp : 0.0);
+      A = nA;
+      C = nC;
     }
-    // 32 independent systems: rows m = lane + 32 t couple m -/+ 32
-    double cp = 0.0, dp = 0.0;
-    for (int m = lane; m < n; m += 32) {
-      const double inv = frcp(1.0 - Ai[m] * cp);
-      cp = Ci[m] * inv;
-      dp = (Di[m] - Ai[m] * dp) * inv;
-      Ci[m] = cp;
-      Di[m] = dp;
-    }
-    const int last = lane + 32 * ((n - 1 - lane) / 32);
-    double x = 0.0;
-    if (lane < n) {
-      for (int m = last; m >= 0; m -= 32) {
-        x = (m == last) ? Di[m] : Di[m] - Ci[m] * x;
-        Di[m] = x;
-      }
+    const double gl = D * frcp(B);
+    const double glm = __shfl_up_sync(0xffffffffu, gl, 1);
+    // 4. back-fill
+    if (lane < nact) {
+      const double gprev = lane ? glm : 0.0;
+      for (int t = 0; t + 1 < m; ++t) RH[o + t] = RH[o + t] + LO[o + t] * gprev + UP[o + t] * gl;
+      RH[o + m - 1] = gl;
     }
     __syncwarp();
     if (FINAL) {
       double* __restrict__ psi = a.psi + po;
       const double w0 = omega(g, rnode<K>(g, i), snode<K>(g, j));
-      for (int m = lane; m < n; m += 32) {
-        const double v = Di[m];
-        psi[base + m] += v;
+      for (int e = lane; e < n; e += 32) {
+        const double v = RH[slot(e)];
+        psi[base + e] += v;
         wsum += w0 * v * v;
       }
     } else {
-      for (int m = lane; m < n; m += 32) R[base + m] = Di[m];
+      for (int e = lane; e < n; e += 32) R[base + e] = RH[slot(e)];
     }
   }
   if (FINAL) {
@@ -457,64 +562,62 @@ template <int S>
 __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
-  const int patch = blockIdx.z / g.nr;
-  const int i = blockIdx.z % g.nr;
+  const int nz = (g.nr + 3) / 4;
+  const int patch = blockIdx.z / nz, i0 = 4 * (blockIdx.z % nz);
   double w = 0.0;
-  if (k < g.np && solved<KC>(g, i, j, k)) {
+  if (k >= 1 && k <= g.np - 2 && j >= 1 && j <= g.nt - 2) {
     const long long pc = patch * psize(g, KC);
     const long long orr = patch * psize(g, KR), ot = patch * psize(g, KT), op = patch * psize(g, KP);
     const double *uri = a.urit + orr, *urn = a.urn + orr;
     const double *uti = a.utit + ot, *utn = a.utn + ot;
     const double *upi = a.upit + op, *upn = a.upn + op;
-    const double rn = __ldg(g.rc + i), sn = __ldg(g.sc + j);
-    const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1);
-    const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1);
-    const double rs = __ldg(g.ir_c + i) * __ldg(g.is_c + j);
-    const double ur0 = 0.5 * (uri[IX<KR>(g, i, j, k)] + urn[IX<KR>(g, i, j, k)]);
-    const double ur1 = 0.5 * (uri[IX<KR>(g, i + 1, j, k)] + urn[IX<KR>(g, i + 1, j, k)]);
-    const double ut0 = 0.5 * (uti[IX<KT>(g, i, j, k)] + utn[IX<KT>(g, i, j, k)]);
-    const double ut1 = 0.5 * (uti[IX<KT>(g, i, j + 1, k)] + utn[IX<KT>(g, i, j + 1, k)]);
-    const double up0 = 0.5 * (upi[IX<KP>(g, i, j, k)] + upn[IX<KP>(g, i, j, k)]);
-    const double up1 = 0.5 * (upi[IX<KP>(g, i, j, k + 1)] + upn[IX<KP>(g, i, j, k + 1)]);
-    const double dv = (f1 * ur1 - f0 * ur0) * __ldg(g.idv1_c + i) + (s1 * ut1 - s0 * ut0) * (rs * g.idth) +
-                      (up1 - up0) * (rs * g.idph);
-    const long long q = pc + IX<KC>(g, i, j, k);
-    double nv;
-    if (S == 1) nv = a.pn[q] - g.inv_chi * dv;
-    else nv = a.pn[q] + (a.p1it[q] - a.p1n[q]) - g.inv_chi * dv;
-    const double d = nv - a.pit[q];
-    a.pit[q] = nv;
-    w = omega(g, rn, sn) * d * d;
+    const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1), sn = __ldg(g.sc + j), is = __ldg(g.is_c + j);
+    for (int i = i0; i < i0 + 4 && i < g.nr; ++i) {
+      const double ir = __ldg(g.ir_c + i);
+      const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1);
+      const double ur0 = 0.5 * (uri[IX<KR>(g, i, j, k)] + urn[IX<KR>(g, i, j, k)]);
+      const double ur1 = 0.5 * (uri[IX<KR>(g, i + 1, j, k)] + urn[IX<KR>(g, i + 1, j, k)]);
+      const double ut0 = 0.5 * (uti[IX<KT>(g, i, j, k)] + utn[IX<KT>(g, i, j, k)]);
+      const double ut1 = 0.5 * (uti[IX<KT>(g, i, j + 1, k)] + utn[IX<KT>(g, i, j + 1, k)]);
+      const double up0 = 0.5 * (upi[IX<KP>(g, i, j, k)] + upn[IX<KP>(g, i, j, k)]);
+      const double up1 = 0.5 * (upi[IX<KP>(g, i, j, k + 1)] + upn[IX<KP>(g, i, j, k + 1)]);
+      const double dv = (f1 * ur1 - f0 * ur0) * __ldg(g.idv1_c + i) + (s1 * ut1 - s0 * ut0) * (ir * is * g.idth) +
+                        (up1 - up0) * (ir * is * g.idph);
+      const long long q = pc + IX<KC>(g, i, j, k);
+      double nv;
+      if (S == 1) nv = a.pn[q] - g.inv_chi * dv;
+      else nv = a.pn[q] + (a.p1it[q] - a.p1n[q]) - g.inv_chi * dv;
+      const double d = nv - a.pit[q];
+      a.pit[q] = nv;
+      w += omega(g, __ldg(g.rc + i), sn) * d * d;
+    }
   }
   const double t = block_sum<128>(w);
-  if (threadIdx.x == 0) {
-    const int b = (blockIdx.z % g.nr) * gridDim.y * gridDim.x + blockIdx.y * gridDim.x + blockIdx.x;
-    a.part[(long long)(blockIdx.z / g.nr) * a.maxb + b] = t;
-  }
+  if (threadIdx.x == 0)
+    a.part[(long long)patch * a.maxb + ((blockIdx.z % nz) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
 }
 
 // ---------------------------------------------------------------------------------
 // K6: deterministic final reduction: 18 (quantity, patch) sums in fixed order,
 // rho = max sqrt; NaN/Inf -> flag.
 // ---------------------------------------------------------------------------------
-__global__ void k_reduce(const double* __restrict__ part, ReduceArgs a, double* __restrict__ out) {
-  const int w = threadIdx.x / 32, l = threadIdx.x % 32;   // one warp per (slot, patch)
-  __shared__ double sums[2 * NSLOT];
-  if (w < 2 * NSLOT) {
-    const int slot = w / 2, patch = w % 2;
-    const double* p = part + ((long long)slot * 2 + patch) * a.maxb;
-    const int nb = a.nblk[slot];
-    double v = 0.0;
-    for (int b = l; b < nb; b += 32) v += p[b];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (l == 0) sums[w] = v;
-  }
-  __syncthreads();
+__global__ void __launch_bounds__(256) k_reduce_slots(const double* __restrict__ part, ReduceArgs a,
+                                                      double* __restrict__ out) {
+  const int slot = blockIdx.x / 2, patch = blockIdx.x % 2;   // one block per (slot, patch)
+  const double* p = part + ((long long)slot * 2 + patch) * a.maxb;
+  const int nb = a.nblk[slot];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += p[b];
+  const double t = block_sum<256>(v);
+  if (threadIdx.x == 0) out[2 + blockIdx.x] = t;
+}
+
+__global__ void k_reduce_final(double* __restrict__ out) {
   if (threadIdx.x == 0) {
     double rho = 0.0;
     int bad = 0;
     for (int q = 0; q < 2 * NSLOT; ++q) {
-      const double s = sums[q];
+      const double s = out[2 + q];
       if (!(s == s) || s > 1e300) bad = 1;
       out[2 + q] = sqrt(s);
       rho = fmax(rho, sqrt(s));
@@ -620,7 +723,8 @@ template <int Q, bool F>
 static int sweep_phi(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   const int n = NPk(g, K) - 2;
-  const size_t per_warp = (size_t)6 * n * sizeof(double);
+  const int Mp = ((n + 31) / 32) | 1;
+  const size_t per_warp = (size_t)3 * 32 * Mp * sizeof(double);
   int nw = (int)((200 * 1024) / per_warp);   // <= 227 KB opt-in per block on sm_100
   nw = nw < 1 ? 1 : (nw > 4 ? 4 : nw);
   const long long lines = (long long)((K == KR) ? g.nr - 1 : g.nr) * (NTk(g, K) - 2);
@@ -639,11 +743,27 @@ template <int Q, int AX, bool F>
 static int sweep_one(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   if (AX == 2) return sweep_phi<Q, F>(g, a, npatch, st);
+  // line length; c' lives in shared memory (64 lines per block) when it fits
+  const int n = (AX == 0) ? ((K == KR) ? g.nr - 1 : g.nr) : NTk(g, K) - 2;
+  const int tpb = 64;
+  const size_t smem = (size_t)n * tpb * sizeof(double);
+  // measured on B200 (C3): shared-memory c' halves occupancy and is ~2x slower
+  // than the high-occupancy version with c' in L2/global scratch; kept off
+  const bool smc = false && smem <= 100 * 1024;
+  const int bx = smc ? tpb : 128;
   dim3 grid;
-  if (AX == 0) grid = dim3((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, npatch);
-  else if (AX == 1) grid = dim3((NPk(g, K) - 2 + 127) / 128, (K == KR ? g.nr - 1 : g.nr), npatch);
-  else grid = dim3((NTk(g, K) - 2 + 127) / 128, (K == KR ? g.nr - 1 : g.nr), npatch);
-  k_sweep<Q, AX, F><<<grid, 128, 0, st>>>(g, a);
+  if (AX == 0) grid = dim3((NPk(g, K) - 2 + bx - 1) / bx, NTk(g, K) - 2, npatch);
+  else grid = dim3((NPk(g, K) - 2 + bx - 1) / bx, (K == KR ? g.nr - 1 : g.nr), npatch);
+  if (smc) {
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      cudaFuncSetAttribute(k_sweep<Q, AX, F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    k_sweep<Q, AX, F, true><<<grid, tpb, smem, st>>>(g, a);
+  } else {
+    k_sweep<Q, AX, F, false><<<grid, 128, 0, st>>>(g, a);
+  }
   return (int)(grid.x * grid.y);
 }
 
@@ -664,14 +784,16 @@ int launch_sweep(const Geo& g, int q, int ax, bool fin, const SweepArgs& a, int 
 }
 
 int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st) {
-  dim3 grid = pgrid(g, KC, 2);
+  const int nz = (g.nr + 3) / 4;
+  dim3 grid((g.np + 127) / 128, g.nt, 2 * nz);
   if (s == 1) k_pres<1><<<grid, 128, 0, st>>>(g, a);
   else k_pres<2><<<grid, 128, 0, st>>>(g, a);
-  return (int)(grid.x * grid.y * g.nr);
+  return (int)(grid.x * grid.y * nz);
 }
 
 void launch_reduce(const double* part, const ReduceArgs& a, double* out, cudaStream_t st) {
-  k_reduce<<<1, 32 * 2 * NSLOT, 0, st>>>(part, a, out);
+  k_reduce_slots<<<2 * NSLOT, 256, 0, st>>>(part, a, out);
+  k_reduce_final<<<1, 32, 0, st>>>(out);
 }
 
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st) {
