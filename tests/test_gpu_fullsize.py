@@ -1,0 +1,96 @@
+"""GPU parity at the BASELINE.json full sizes, in the launch configuration
+bench.py times.
+
+* C2 / C3 / C5 first time step against tests/golden/<cfg>_step1.json, written by
+  tools/make_golden.py from the CPU oracle alone: identical Schwarz iteration
+  count and every sampled node within 1e-11 (DESIGN.md RD-E3 metric).
+* C3 static right-hand sides G_q (all solved nodes) against oracle.static().
+* C4 kernel-only line solves (256x384x1152, every line of every axis) against
+  the oracle's Thomas sweep.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _shell(cfg, **kw):
+    from paper_1905_02300_b200 import Shell
+    return Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, **kw)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_first_step_matches_oracle_golden(name):
+    path = os.path.join(GOLD, f"{name.lower()}_step1.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet (tools/make_golden.py {name})")
+    gold = json.load(open(path))
+    cfg = W.config(name)
+    assert gold["grid"] == [cfg.nr, cfg.nth, cfg.nph]
+    sh = _shell(cfg)
+    sh.load_workload(W.make_workload(cfg))
+    sh.step(1, cfg.tol)
+    k, rho = sh.stats()[-1]
+    assert k == gold["schwarz_iters"], (k, gold["schwarz_iters"], rho, gold["rho"])
+    worst = 0.0
+    for p in range(2):
+        for s in (1, 2):
+            f = sh.get_fields(p, 0, s)
+            vmax = max(gold["samples"][f"{p}/{s}/{q}"]["absmax"] for q in ("ur", "ut", "up"))
+            for q, arr in f.items():
+                g = gold["samples"][f"{p}/{s}/{q}"]
+                den = vmax if q in ("ur", "ut", "up") else g["absmax"]
+                got = np.array([arr[tuple(i)] for i in g["index"]])
+                e = float(np.max(np.abs(got - np.array(g["value"])))) / den
+                worst = max(worst, e)
+    assert worst <= 1e-11, worst
+
+
+def test_c3_static_rhs_full_size():
+    from oracle.scheme import Oracle
+    cfg = W.config("C3")
+    wl = W.make_workload(cfg)
+    sh = _shell(cfg, fixed_iters=1)
+    sh.load_workload(wl)
+    sh.step(1, cfg.tol)
+    o = Oracle(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    o.load_workload(wl)
+    for p in range(2):
+        astar, G = o.static(p, 0.0)
+        for q, kind in (("T", "C"), ("ur1", "R"), ("ut2", "TH"), ("up2", "PH")):
+            m = o.g.solved_mask(kind)
+            a = sh.debug_get("G_" + q, p)[m]
+            b = G[q][m]
+            scale = max(np.max(np.abs(b)), 1e-300)
+            assert np.max(np.abs(a - b)) <= 1e-12 * scale, (p, q)
+        del astar, G
+
+
+def test_c4_line_solves_full_size():
+    import torch
+    from oracle import ops
+    from oracle.scheme import Oracle
+    nr, nt, npp = 256, 384, 1152
+    a, rhs = W.c4_inputs(nr, nt, npp)
+    cfg = W.Config("C4", nr, nt, npp, dt=1e-4)
+    sh = _shell(cfg)
+    o = Oracle(nr, nt, npp, 1.0, 2.0, 1.0, 0.0, 1e-4)
+    astar = [a["ur"], a["ut"], a["up"]]
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    dar, dat, dap = dev(a["ur"]), dev(a["ut"]), dev(a["up"])
+    m = o.g.solved_mask("C")
+    for axis in range(3):
+        x = dev(rhs)
+        sh.line_solve(axis, dar, dat, dap, x)
+        torch.cuda.synchronize()
+        got = x.cpu().numpy()
+        ref = o.sweep("T", rhs, axis, ops.coeffs(o.g, o.prm, "T", axis, True, astar))
+        err = np.max(np.abs(got[m] - ref[m])) / np.max(np.abs(ref[m]))
+        assert err <= 1e-13, (axis, err)
+        del got, ref, x
