@@ -280,8 +280,11 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
 // In place on R (d' then x); c' in scratch C.  FINAL: psi += x and norm partial.
 // Line grid: AX=0: x -> k, y -> j;  AX=1: x -> k, y -> i;  AX=2: x -> j, y -> i.  z -> patch.
 // ---------------------------------------------------------------------------------
+
 template <int Q, int AX, bool FINAL, bool SMC>
 __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
+  // rows per load round (measured on B200, C3: 4 best for r-lines, 8 for theta-lines)
+  constexpr int SB = (AX == 0) ? 4 : 8;
   extern __shared__ double csm[];   // SMC: c' column of this thread at csm[m * blockDim.x + threadIdx.x]
   constexpr int K = kind_of(Q);
   const int patch = blockIdx.z;
@@ -320,12 +323,12 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
     double cprev = 0.0, dprev = 0.0;
     // forward elimination, 4 rows per round: the round's loads (rhs and the
     // read-only a* / table loads inside coef) are all issued before use
-    for (int m0 = 0; m0 < n; m0 += 4) {
-      double rv[4], am[4], a0[4], ap[4];
+    for (int m0 = 0; m0 < n; m0 += SB) {
+      double rv[SB], am[SB], a0[SB], ap[SB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) rv[u] = (m0 + u < n) ? R[base + (m0 + u) * stride] : 0.0;
+      for (int u = 0; u < SB; ++u) rv[u] = (m0 + u < n) ? R[base + (m0 + u) * stride] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SB; ++u) {
         const int m = m0 + u;
         if (m < n) {
           const int ii = (AX == 0) ? i + m : i, jj = (AX == 1) ? j + m : j, kk = (AX == 2) ? k + m : k;
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SB; ++u) {
         const int m = m0 + u;
         if (m < n) {
           double di = 1.0 - th * a0[u];
@@ -356,10 +359,10 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
     }
     double x = 0.0;
     double* __restrict__ psi = FINAL ? a.psi + po : nullptr;
-    for (int m0 = n - 1; m0 >= 0; m0 -= 4) {
-      double cv[4], dv[4], pv[4];
+    for (int m0 = n - 1; m0 >= 0; m0 -= SB) {
+      double cv[SB], dv[SB], pv[SB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SB; ++u) {
         const int m = m0 - u;
         if (m >= 0) {
           const long long q = base + m * stride;
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SB; ++u) {
         const int m = m0 - u;
         if (m >= 0) {
           const long long q = base + m * stride;
@@ -406,6 +409,8 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
 //  4. back-fill x, coalesced write-back.
 // Same rows and end conditions as the serial Thomas of k_sweep (x 1e-16 rounding).
 // ---------------------------------------------------------------------------------
+constexpr int PB = 8;   // elements per lane per load round in the phi sweep
+
 template <int Q, bool FINAL>
 __global__ void __launch_bounds__(128) k_sweep_phi(Geo g, SweepArgs a, int nwarps) {
   constexpr int K = kind_of(Q);
@@ -438,20 +443,20 @@ __global__ void __launch_bounds__(128) k_sweep_phi(Geo g, SweepArgs a, int nwarp
     };
     // 1. rows (I - tau/2 A_ph) of this line; 4 elements per lane per round so
     //    that all of a round's loads are in flight before any is consumed
-    for (int e0 = lane; e0 < n; e0 += 128) {
-      double rv[4], am[4], a0[4], ap[4];
+    for (int e0 = lane; e0 < n; e0 += 32 * PB) {
+      double rv[PB], am[PB], a0[PB], ap[PB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PB; ++u) {
         const int e = e0 + 32 * u;
         rv[u] = (e < n) ? R[base + e] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PB; ++u) {
         const int e = e0 + 32 * u;
         if (e < n) coef<Q, 2, true>(g, As, i, j, 1 + e, am[u], a0[u], ap[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PB; ++u) {
         const int e = e0 + 32 * u;
         if (e < n) {
           const int q = slot(e);
