@@ -521,6 +521,8 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   if (!out) return YY_EINVAL;
   *out = nullptr;
   if (!gr || gr->nr < 2 || gr->ntheta < 8 || gr->nphi < 8) return YY_EINVAL;
+  // per-patch offsets are 32-bit in the kernels
+  if ((double)(gr->nr + 1) * (gr->ntheta + 1) * (gr->nphi + 1) >= 2147483647.0) return YY_EINVAL;
   if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
   yy_ctx* ctx = new yy_ctx();
   ctx->R1 = R1; ctx->R2 = R2; ctx->Pr = Pr; ctx->Ra = Ra; ctx->dt = dt;

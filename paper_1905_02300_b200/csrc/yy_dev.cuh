@@ -61,9 +61,11 @@ __host__ __device__ __forceinline__ long long psize(const Geo& g, int K) {
 __host__ __device__ __forceinline__ long long wsize(const Geo& g, int K) {   // one wall (theta x phi)
   return (long long)NTk(g, K) * NPk(g, K);
 }
+// Offset of node (i,j,k) inside ONE patch's array of kind K.  32-bit: the
+// largest per-patch array (C4, 257x385x1153) has 1.1e8 < 2^31 elements.
 template <int K>
-__device__ __forceinline__ long long IX(const Geo& g, int i, int j, int k) {
-  return ((long long)i * NTk(g, K) + j) * NPk(g, K) + k;
+__device__ __forceinline__ int IX(const Geo& g, int i, int j, int k) {
+  return (i * NTk(g, K) + j) * NPk(g, K) + k;
 }
 
 // Transport velocity a* = u2^{*,n+1/2} (RD8), one patch.

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
   if (k >= NPk(g, K) || !solved<K>(g, i, j, k)) return;
   const long long po = patch * psize(g, K);
   const long long pc = patch * psize(g, KC);
-  const long long node = IX<K>(g, i, j, k);
+  const int node = IX<K>(g, i, j, k);
   Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
   const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
   const double* Wm = a.wm ? a.wm + patch * 2 * wsize(g, K) : nullptr;
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
   if (k >= NPk(g, K) || !solved<K>(g, i, j, k)) return;
   const long long po = patch * psize(g, K);
   const long long pc = patch * psize(g, KC);
-  const long long node = IX<K>(g, i, j, k);
+  const int node = IX<K>(g, i, j, k);
   Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
   const double* Wnew = a.wnew ? a.wnew + patch * 2 * wsize(g, K) : nullptr;
   const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
