@@ -16,6 +16,10 @@
 #include "yy_dev.cuh"
 #include "yy_internal.h"
 
+#ifndef YY_BWD_PREFETCH
+#define YY_BWD_PREFETCH 1
+#endif
+
 namespace yy {
 
 // ---------------------------------------------------------------------------------
@@ -85,6 +89,10 @@ __device__ __forceinline__ double div2(const Geo& g, const double* ut, int i, in
 }
 __device__ __forceinline__ double div3(const Geo& g, const double* up, int i, int j, int k) {
   return (up[IX<KP>(g, i, j, k + 1)] - up[IX<KP>(g, i, j, k)]) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
+}
+
+__device__ __forceinline__ void pf_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ double omega(const Geo& g, double r, double s) {
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
 // ---------------------------------------------------------------------------------
 
 template <int Q, int AX, bool FINAL, bool SMC>
-__global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
+__global__ void __launch_bounds__(128, (AX == 1) ? 4 : 7) k_sweep(Geo g, SweepArgs a) {
   // rows per load round (measured on B200, C3: 4 best for r-lines, 8 for theta-lines)
   constexpr int SB = (AX == 0) ? 4 : 8;
   extern __shared__ double csm[];   // SMC: c' column of this thread at csm[m * blockDim.x + threadIdx.x]
@@ -323,7 +331,19 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
     double cprev = 0.0, dprev = 0.0;
     // forward elimination, 4 rows per round: the round's loads (rhs and the
     // read-only a* / table loads inside coef) are all issued before use
+    // L2 prefetch distance (rows) for the inputs of the next rounds
+    const double* pfa = (AX == 0) ? A.ar : A.at;
+    const int pko = (AX == 0) ? IX<KR>(g, i, j, k) : IX<KT>(g, i, j, k);
+    const long long pst = (AX == 0) ? (long long)g.nt * g.np : (long long)g.np;
     for (int m0 = 0; m0 < n; m0 += SB) {
+#pragma unroll
+      for (int u = 0; u < SB; ++u) {
+        const int mp = m0 + 2 * SB + u;
+        if (mp < n) {
+          pf_l2(R + base + mp * stride);
+          pf_l2(pfa + pko + mp * pst);
+        }
+      }
       double rv[SB], am[SB], a0[SB], ap[SB];
 #pragma unroll
       for (int u = 0; u < SB; ++u) rv[u] = (m0 + u < n) ? R[base + (m0 + u) * stride] : 0.0;
@@ -360,6 +380,17 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, SweepArgs a) {
     double x = 0.0;
     double* __restrict__ psi = FINAL ? a.psi + po : nullptr;
     for (int m0 = n - 1; m0 >= 0; m0 -= SB) {
+#if YY_BWD_PREFETCH
+#pragma unroll
+      for (int u = 0; u < SB; ++u) {
+        const int mp = m0 - 2 * SB - u;
+        if (mp >= 0) {
+          pf_l2(Cs + cidx(mp));
+          pf_l2(R + base + mp * stride);
+          if (FINAL) pf_l2(a.psi + po + base + mp * stride);
+        }
+      }
+#endif
       double cv[SB], dv[SB], pv[SB];
 #pragma unroll
       for (int u = 0; u < SB; ++u) {
@@ -747,7 +778,9 @@ static int sweep_phi(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t 
 template <int Q, int AX, bool F>
 static int sweep_one(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
-  if (AX == 2) return sweep_phi<Q, F>(g, a, npatch, st);
+  if constexpr (AX == 2) {
+    return sweep_phi<Q, F>(g, a, npatch, st);
+  } else {
   // line length; c' lives in shared memory (64 lines per block) when it fits
   const int n = (AX == 0) ? ((K == KR) ? g.nr - 1 : g.nr) : NTk(g, K) - 2;
   const int tpb = 64;
@@ -770,6 +803,7 @@ static int sweep_one(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t 
     k_sweep<Q, AX, F, false><<<grid, 128, 0, st>>>(g, a);
   }
   return (int)(grid.x * grid.y);
+  }
 }
 
 template <int Q>
