@@ -108,6 +108,11 @@ QK = {"T": "C", "ur": "R", "ut": "TH", "up": "PH"}
 def m1_bytes(name, cfg, nsrc):
     """Algorithmic bytes of ONE launch of kernel class `name` (both patches)."""
     P = 2
+    if "+resid_" in name:
+        # fused first sweep: the residual's reads + the sweep's own a* reads + one
+        # write (the R round trip of the unfused pair is not moved)
+        sw, rs = name.split("+")
+        return m1_bytes(rs, cfg, nsrc) + m1_bytes(sw, cfg, nsrc) - 8 * P * kind_nodes(cfg, QK[sw.split("_")[1]]) * 2
     if name.startswith("sweep_"):
         _, q, ax = name.split("_")[:3]
         fin = name.endswith("_fin")

@@ -66,7 +66,8 @@ enum {
 };
 
 typedef struct {
-  int32_t nr, ntheta, nphi;   /* cells per patch; ntheta >= 8, nphi >= 8, nr >= 2 */
+  int32_t nr, ntheta, nphi;   /* cells per patch; 2 <= nr <= 512, 8 <= ntheta <= 513, 8 <= nphi <= 1153
+                                 (longest lines of the chunked line solver; larger -> YY_EINVAL) */
 } yy_grid;
 
 typedef struct yy_ctx yy_ctx;

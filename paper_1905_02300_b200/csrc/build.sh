@@ -1,8 +1,21 @@
 #!/bin/bash
 # Build libyy.so for sm_100a (in-tree).  Usage: build.sh [outdir]
+# Translation units compile in parallel; the line-sweep file once per quantity.
 set -e
 HERE="$(cd "$(dirname "$0")" && pwd)"
 OUT="${1:-$HERE/..}"
 NVCC="${NVCC:-/usr/local/cuda/bin/nvcc}"
-FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Xptxas -v"
-"$NVCC" $FLAGS -o "$OUT/libyy.so" "$HERE/yy_api.cu" "$HERE/yy_kernels.cu" 2> "$OUT/.ptxas.log" || { cat "$OUT/.ptxas.log"; exit 1; }
+FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v"
+OBJ="$(mktemp -d)"
+trap 'rm -rf "$OBJ"' EXIT
+pids=()
+"$NVCC" $FLAGS -c -o "$OBJ/api.o" "$HERE/yy_api.cu" 2> "$OBJ/api.log" & pids+=($!)
+"$NVCC" $FLAGS -c -o "$OBJ/kernels.o" "$HERE/yy_kernels.cu" 2> "$OBJ/kernels.log" & pids+=($!)
+for q in 0 1 2 3; do
+  "$NVCC" $FLAGS -DYY_LINE_Q=$q -c -o "$OBJ/line$q.o" "$HERE/yy_line.cu" 2> "$OBJ/line$q.log" & pids+=($!)
+done
+rc=0
+for p in "${pids[@]}"; do wait "$p" || rc=1; done
+cat "$OBJ"/*.log > "$OUT/.ptxas.log"
+if [ $rc -ne 0 ]; then grep -i -B2 -A3 "error" "$OUT/.ptxas.log" | head -60; exit 1; fi
+"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libyy.so" "$OBJ"/*.o

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -43,6 +44,7 @@ struct yy_ctx {
   Geo g{};
   double R1 = 1, R2 = 2, Pr = 1, Ra = 0, dt = 1e-3, chi = 1.0;
   int max_iters = 100, fixed_iters = 0;
+  bool fuse = false;           // residual fused into the first sweep (YY_FUSE=1; measured slower on C3 so far)
   double t = 0.0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -395,8 +397,9 @@ yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
   r.urit = ctx->it[FUR1 + o]; r.urn = ctx->n[FUR1 + o];
   r.utit = ctx->it[FUT1 + o]; r.utn = ctx->n[FUT1 + o];
   r.p1it = ctx->it[FP1]; r.p1n = ctx->n[FP1];
-  {
-    ProfScope ps(ctx, kname(std::string("resid_") + QNAME[q] + (q ? (s == 1 ? "1" : "2") : "")), 1);
+  const std::string rname = std::string("resid_") + QNAME[q] + (q ? (s == 1 ? "1" : "2") : "");
+  if (!ctx->fuse) {
+    ProfScope ps(ctx, kname(rname), 1);
     launch_resid(g, q, s, r, ctx->st);
   }
   SweepArgs w{};
@@ -405,9 +408,12 @@ yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
   w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
   w.maxb = ctx->maxb;
   for (int a = 0; a < 3; ++a) {
-    const bool fin = (a == 2);
-    ProfScope ps(ctx, kname(std::string("sweep_") + QNAME[q] + "_" + AXNAME[ORDER[q][a]] + (fin ? "_fin" : "")), 1);
-    const int nb = launch_sweep(g, q, ORDER[q][a], fin, w, 2, ctx->st);
+    const bool fin = (a == 2), first = (a == 0) && ctx->fuse;
+    // fused first sweep: class "sweep_<q>_<ax>+resid_<q><s>"
+    ProfScope ps(ctx, kname(std::string("sweep_") + QNAME[q] + "_" + AXNAME[ORDER[q][a]] + (fin ? "_fin" : "") +
+                            (first ? "+" + rname : "")), 1);
+    const int nb = launch_sweep(g, q, ORDER[q][a], s, first, fin, w, first ? &r : nullptr, 2, ctx->st);
+    if (nb < 0) return fail(ctx, YY_ESTATE, "internal: no sweep kernel for this factor");
     if (fin) nblk[slot] = nb;
   }
   return YY_OK;
@@ -521,10 +527,13 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   if (!out) return YY_EINVAL;
   *out = nullptr;
   if (!gr || gr->nr < 2 || gr->ntheta < 8 || gr->nphi < 8) return YY_EINVAL;
+  // longest lines the register-chunked line solver takes (yy_line.cu)
+  if (gr->nr > max_line_len(0) || gr->ntheta - 1 > max_line_len(1) || gr->nphi - 1 > max_line_len(2)) return YY_EINVAL;
   // per-patch offsets are 32-bit in the kernels
   if ((double)(gr->nr + 1) * (gr->ntheta + 1) * (gr->nphi + 1) >= 2147483647.0) return YY_EINVAL;
   if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
   yy_ctx* ctx = new yy_ctx();
+  if (const char* e = std::getenv("YY_FUSE")) ctx->fuse = (e[0] && e[0] != '0');
   ctx->R1 = R1; ctx->R2 = R2; ctx->Pr = Pr; ctx->Ra = Ra; ctx->dt = dt;
   HostGeo h = host_geo(gr, R1, R2);
   Geo& g = ctx->g;
@@ -621,6 +630,8 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   for (int K = 0; K < 4; ++K) {
     mb = std::max(mb, (long long)((NPk(g, K) + 127) / 128) * NTk(g, K) * NRk(g, K));
     mb = std::max(mb, (long long)((NTk(g, K) + 127) / 128) * NRk(g, K));
+    mb = std::max(mb, (long long)((NPk(g, K) + 3) / 4) * std::max(NTk(g, K), NRk(g, K)));   // r/theta line tiles
+    mb = std::max(mb, (long long)NRk(g, K) * NTk(g, K));                                     // phi line tiles
   }
   ctx->maxb = (int)mb;
   if ((s = dalloc(ctx, &ctx->part, (size_t)NSLOT * 2 * mb)) != YY_OK || (s = dalloc(ctx, &ctx->red, 2 + 2 * NSLOT)) != YY_OK) { yy_destroy(ctx); return s; }
@@ -823,7 +834,7 @@ extern "C" yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar
   SweepArgs w{};
   w.ar = d_ar; w.at = d_at; w.ap = d_ap;
   w.R = d_x; w.C = ctx->C; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
-  launch_sweep(ctx->g, QT, axis, false, w, 1, ctx->st);
+  launch_sweep(ctx->g, QT, axis, 1, false, false, w, nullptr, 1, ctx->st);
   CK(cudaGetLastError());
   return YY_OK;
 }

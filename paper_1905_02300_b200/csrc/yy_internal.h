@@ -94,7 +94,25 @@ struct InterpArgs {
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);
 void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st);
 void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t st);
-int launch_sweep(const Geo& g, int q, int ax, bool fin, const SweepArgs& a, int npatch, cudaStream_t st);
+inline int max_line_len(int ax) { return ax == 2 ? 32 * 36 : 32 * 16; }   // unknowns per line (yy_line.cu)
+// line sweeps (yy_line.cu): factor `ax` of quantity Q, system s; first = fused
+// eq:er residual from *ra (the quantity's first factor), fin = psi += x and the
+// norm partial (its last factor); neither = plain.  Returns blocks launched
+// (norm partial count) or -1 if (ax, first, fin) is not a factor position of Q.
+template <int Q>
+int launch_sweep_q(const Geo& g, int ax, int s, bool first, bool fin, const SweepArgs& a, const ResidArgs* ra,
+                   int npatch, cudaStream_t st);
+#ifndef YY_LINE_Q   // (the per-quantity line TUs instantiate only their own Q)
+inline int launch_sweep(const Geo& g, int q, int ax, int s, bool first, bool fin, const SweepArgs& a,
+                        const ResidArgs* ra, int npatch, cudaStream_t st) {
+  switch (q) {
+    case 0: return launch_sweep_q<0>(g, ax, s, first, fin, a, ra, npatch, st);
+    case 1: return launch_sweep_q<1>(g, ax, s, first, fin, a, ra, npatch, st);
+    case 2: return launch_sweep_q<2>(g, ax, s, first, fin, a, ra, npatch, st);
+    default: return launch_sweep_q<3>(g, ax, s, first, fin, a, ra, npatch, st);
+  }
+}
+#endif
 int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st);
 void launch_reduce(const double* part, const ReduceArgs& a, double* out, cudaStream_t st);
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st);

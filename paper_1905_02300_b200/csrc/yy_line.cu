@@ -1,0 +1,418 @@
+// yy_line.cu — the implicit factor sweeps of the Yin-Yang AC direction-splitting
+// step (arXiv 1905.02300): on every line of one axis solve
+//     (I - tau/2 A_{Q,AX}) x = b
+// (the factors of eq:Convect_Douglas L318-325, eq:r_comp L398-401, eq:theta_comp
+// L423-425, eq:phi_comp L447-449; homogeneous increments, wall ghost RD23).
+//
+// One design for the three axes: a line of n rows is split into P contiguous
+// chunks of M rows (P*M >= n; rows past n are identity rows), one chunk per
+// thread, the P threads of a line forming an aligned segment of a warp.  Every
+// thread keeps its chunk in REGISTERS and
+//   1. builds its rows (normalised by the diagonal) from b and the transport
+//      velocity a*  (coef<> of yy_dev.cuh, the rows the residual applies);
+//   2. eliminates the chunk interior with the chunk's last unknown g_c and the
+//      previous chunk's g_{c-1} kept symbolic: x_t = y_t + v_t g_{c-1} + w_t g_c
+//      (one reciprocal per row) — the Schur-complement partition of the
+//      distributed tridiagonal solve of P:L477-480, here across warp lanes;
+//   3. solves the P-unknown interface system by log2(P) steps of parallel
+//      cyclic reduction over segment shuffles;
+//   4. back-fills x and writes it (or psi += x and the convergence norm, FINAL).
+// No shared-memory round trips and no c'/d' scratch in HBM: an r or theta line
+// costs exactly its algorithmic bytes (read b, read a*, write x).
+//
+// r and theta lines (strided): a warp covers 32/P consecutive phi-lines, so a
+// load of row t touches P segments of 256/P contiguous bytes (full sectors).
+// phi lines (contiguous): the rows are built coalesced into shared memory in
+// chunk-major layout (odd pitch, conflict-free), then read back per chunk.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "yy_dev.cuh"
+#include "yy_internal.h"
+#include "yy_stencil.cuh"
+
+namespace yy {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Steps 2-4 on registers: rows lo_t x_{t-1} + x_t + up_t x_{t+1} = rh_t of this
+// thread's chunk c (0..P-1) of its line.  On exit rh[t] = x_t.
+template <int P, int M>
+__device__ __forceinline__ void part_solve(double (&lo)[M], double (&up)[M], double (&rh)[M], int c) {
+  static_assert(M >= 2, "chunk of at least two rows");
+  // forward over the interior rows 0..M-2:  x_t + c'_t x_{t+1} = y'_t + v'_t g_{c-1}
+  double cp = 0.0, yp = 0.0, vp = 0.0;
+#pragma unroll
+  for (int t = 0; t < M - 1; ++t) {
+    const double l = lo[t];
+    if (t == 0) {
+      cp = up[0];
+      yp = rh[0];
+      vp = -l;
+    } else {
+      const double inv = frcp(1.0 - l * cp);
+      cp = up[t] * inv;
+      yp = (rh[t] - l * yp) * inv;
+      vp = -l * vp * inv;
+    }
+    up[t] = cp;
+    rh[t] = yp;
+    lo[t] = vp;
+  }
+  // backward: x_t = y_t + v_t g_{c-1} + w_t g_c  (y -> rh, v -> lo, w -> up)
+  {
+    double y = rh[M - 2], v = lo[M - 2], w = -up[M - 2];
+    up[M - 2] = w;
+#pragma unroll
+    for (int t = M - 3; t >= 0; --t) {
+      const double ct = up[t];
+      y = rh[t] - ct * y;
+      v = lo[t] - ct * v;
+      w = -ct * w;
+      rh[t] = y;
+      lo[t] = v;
+      up[t] = w;
+    }
+  }
+  // interface row M-1 of every chunk: A g_{c-1} + B g_c + C g_{c+1} = D,
+  // x_M (first row of chunk c+1) = Y0n + V0n g_c + W0n g_{c+1}
+  const double Y0n = __shfl_down_sync(FULL, rh[0], 1, P);
+  const double V0n = __shfl_down_sync(FULL, lo[0], 1, P);
+  const double W0n = __shfl_down_sync(FULL, up[0], 1, P);
+  const double ae = lo[M - 1], ce = up[M - 1];     // ce = 0 on a line's last row (and identity rows)
+  double A = ae * lo[M - 2];
+  double B = ae * up[M - 2] + 1.0 + ce * V0n;
+  double C = ce * W0n;
+  double D = rh[M - 1] - ae * rh[M - 2] - ce * Y0n;
+#pragma unroll
+  for (int s = 1; s < P; s <<= 1) {
+    const double Am = __shfl_up_sync(FULL, A, s, P), Bm = __shfl_up_sync(FULL, B, s, P);
+    const double Cm = __shfl_up_sync(FULL, C, s, P), Dm = __shfl_up_sync(FULL, D, s, P);
+    const double Ap = __shfl_down_sync(FULL, A, s, P), Bp = __shfl_down_sync(FULL, B, s, P);
+    const double Cp = __shfl_down_sync(FULL, C, s, P), Dp = __shfl_down_sync(FULL, D, s, P);
+    const bool hm = c >= s, hp = c + s < P;
+    const double al = hm ? -A * frcp(Bm) : 0.0;
+    const double ga = hp ? -C * frcp(Bp) : 0.0;
+    const double nA = hm ? al * Am : 0.0;
+    const double nC = hp ? ga * Cp : 0.0;
+    B = B + (hm ? al * Cm : 0.0) + (hp ? ga * Ap : 0.0);
+    D = D + (hm ? al * Dm : 0.0) + (hp ? ga * Dp : 0.0);
+    A = nA;
+    C = nC;
+  }
+  const double gc = D * frcp(B);
+  const double gp = __shfl_up_sync(FULL, gc, 1, P);
+  const double gm = c ? gp : 0.0;
+#pragma unroll
+  for (int t = 0; t < M - 1; ++t) rh[t] = rh[t] + lo[t] * gm + up[t] * gc;
+  rh[M - 1] = gc;
+}
+
+// normalised row m (0..n-1) of the factor at node (i,j,k); rv = right-hand side
+template <int Q, int AX>
+__device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, int j, int k, int m, int n,
+                                         double rv, double& lo, double& up, double& rh) {
+  constexpr int K = kind_of(Q);
+  const double th = 0.5 * g.tau;
+  double am, a0, ap;
+  coef<Q, AX, true>(g, A, i, j, k, am, a0, ap);
+  double di = 1.0 - th * a0;
+  if (AX == 0 && K != KR) {          // antisymmetric wall ghost of the increment (RD23)
+    if (m == 0) di = 1.0 - th * (a0 - am);
+    if (m == n - 1) di = 1.0 - th * (a0 - ap);
+  }
+  const double inv = frcp(di);
+  lo = (m == 0) ? 0.0 : -th * am * inv;
+  up = (m == n - 1) ? 0.0 : -th * ap * inv;
+  rh = rv * inv;
+}
+
+// odd line pitch (>= P*MP) of the chunk-major shared-memory tile: rows of 128/P
+// consecutive lines are stored conflict-free in the build phase of r/theta tiles
+// (lane = line), and chunk reads of the solve phase are <= 2-way conflicted.
+template <int P, int MP>
+__host__ __device__ constexpr int line_pitch() {
+  int best = P * MP + 1, bdeg = 99;
+  for (int LP = P * MP + 1; LP < P * MP + 64; LP += 2) {
+    int deg = 1;
+    for (int h = 0; h < 32; h += 16) {
+      int cnt[16] = {};
+      for (int t = h; t < h + 16; ++t) {
+        const int a = ((t / P) * LP + (t % P) * MP) % 16;
+        if (++cnt[a] > deg) deg = cnt[a];
+      }
+    }
+    if (deg < bdeg) { bdeg = deg; best = LP; }
+  }
+  return best;
+}
+
+// ---------------------------------------------------------------------------------
+// One kernel for the three axes.  A block (128 threads) owns NL = 128/P lines:
+//   AX=0 (r) / AX=1 (theta): NL consecutive k at fixed j / i   (grid x: k tile, y: j / i)
+//   AX=2 (phi): NL consecutive lines (i, j), j fastest          (grid x: line tile)
+// grid z / y: patch.
+// 1. build: M elements per thread (mapping below), coalesced; every thread
+//    issues all its M loads before using any;
+// 2.-3. thread (line q / P, chunk q % P) solves its chunk in registers;
+// 4. write back with the build mapping (FINAL: psi += x and the norm partial).
+// ---------------------------------------------------------------------------------
+enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2 };
+
+template <int Q, int AX, int MODE, int S, int P, int M>
+__global__ void __launch_bounds__(128) k_line(Geo g, SweepArgs a, ResidArgs ra) {
+  constexpr bool FINAL = (MODE == MODE_FINAL);
+  constexpr int K = kind_of(Q);
+  constexpr int NL = 128 / P;
+  constexpr int MP = M | 1;
+  constexpr int LP = line_pitch<P, MP>();
+  constexpr int LN = P * M;                // padded line length
+  extern __shared__ double sm[];
+  double* LO = sm;
+  double* UP = LO + NL * LP;
+  double* RH = UP + NL * LP;
+  const int patch = (AX == 2) ? blockIdx.y : blockIdx.z;
+  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>() + 1 : (AX == 1) ? NTk(g, K) - 2 : NPk(g, K) - 2;
+  const long long po = patch * psize(g, K);
+  const Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+  double* __restrict__ R = a.R + po;
+  // Element u (< M) of this thread in the build / write-back phases:
+  //  r/theta: line l = t % NL (consecutive threads = consecutive k, coalesced),
+  //           rows e = c M + u of chunk c = t / NL (a thread walks its chunk);
+  //  phi:     line l = u / (M/4), row e = t + 128 (u % (M/4)) (coalesced along the line).
+  // Out-of-range elements (ragged tile / padded rows) re-read a valid node and
+  // become identity rows: no load sits behind a branch.
+  constexpr int UPL = M / 4;              // phi: elements per thread per line (LN = 128 UPL)
+  static_assert(AX != 2 || M % 4 == 0, "phi chunks: M multiple of 4");
+  int lt, c1, nlines, L0, stride, i0 = 0, j0 = 0, k0 = 0, nd0 = 0;
+  __shared__ int s_i[AX == 2 ? NL : 1], s_j[AX == 2 ? NL : 1], s_nd[AX == 2 ? NL : 1];
+  if (AX == 2) {
+    const int nj = NTk(g, K) - 2;
+    nlines = ((K == KR) ? g.nr - 1 : g.nr) * nj;
+    L0 = blockIdx.x * NL;
+    if (threadIdx.x < NL) {
+      const int L = min(L0 + (int)threadIdx.x, nlines - 1);   // clamped: a ragged tile reads valid nodes
+      const int ii = i_lo<K>() + L / nj, jj = 1 + L % nj;
+      s_i[threadIdx.x] = ii;
+      s_j[threadIdx.x] = jj;
+      s_nd[threadIdx.x] = IX<K>(g, ii, jj, 1);
+    }
+    __syncthreads();
+    lt = 0;
+    c1 = 0;
+    stride = 1;
+  } else {
+    lt = threadIdx.x % NL;
+    c1 = threadIdx.x / NL;
+    L0 = blockIdx.x * NL + 1;             // first k of the tile
+    nlines = NPk(g, K) - 2 - L0 + 1;      // lines of this tile that exist (may exceed NL)
+    k0 = L0 + min(lt, nlines - 1);
+    if (AX == 0) { i0 = i_lo<K>(); j0 = blockIdx.y + 1; stride = NTk(g, K) * NPk(g, K); }
+    else { i0 = blockIdx.y + i_lo<K>(); j0 = 1; stride = NPk(g, K); }
+    nd0 = IX<K>(g, i0, j0, k0);
+  }
+  const bool lvalid = (AX == 2) || lt < nlines;
+  auto elem = [&](int u, int& l, int& e) {
+    if (AX == 2) { l = u / UPL; e = threadIdx.x + 128 * (u % UPL); }
+    else { l = lt; e = c1 * M + u; }
+  };
+  auto exists = [&](int l, int e) { return e < n && (AX == 2 ? L0 + l < nlines : lvalid); };
+  auto node = [&](int l, int e, int& i, int& j, int& k) {   // l, e clamped by the caller
+    if (AX == 0) { i = i0 + e; j = j0; k = k0; return nd0 + e * stride; }
+    if (AX == 1) { i = i0; j = j0 + e; k = k0; return nd0 + e * stride; }
+    i = s_i[l]; j = s_j[l]; k = 1 + e;
+    return s_nd[l] + e;
+  };
+  auto slot = [&](int l, int e) { return l * LP + (e / M) * MP + (e % M); };
+  // 1. build
+  if (MODE == MODE_FIRST) {
+    // fused eq:er residual: one element at a time (its stencil loads are many and
+    // mostly L1 hits of neighbouring threads); occupancy hides the latency
+#pragma unroll 2
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      const int ec = min(e, n - 1);
+      node(l, ec, i, j, k);
+      const double rv = resid_at<Q, S>(g, ra, patch, i, j, k);
+      double lo, up, rh;
+      make_row<Q, AX>(g, A, i, j, k, ec, n, rv, lo, up, rh);
+      const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
+      const int s = slot(l, e);
+      LO[s] = lo * mk;
+      UP[s] = up * mk;
+      RH[s] = rh * mk;
+    }
+  } else {
+    double rv[M];
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      rv[u] = R[node(l, min(e, n - 1), i, j, k)];
+    }
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      const int ec = min(e, n - 1);
+      node(l, ec, i, j, k);
+      double lo, up, rh;
+      make_row<Q, AX>(g, A, i, j, k, ec, n, rv[u], lo, up, rh);
+      const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
+      const int s = slot(l, e);
+      LO[s] = lo * mk;
+      UP[s] = up * mk;
+      RH[s] = rh * mk;
+    }
+  }
+  __syncthreads();
+  // 2.-3. solve chunk c of line l
+  {
+    const int l = threadIdx.x / P, c = threadIdx.x % P;
+    const int o = l * LP + c * MP;
+    double lo[M], up[M], rh[M];
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      lo[u] = LO[o + u];
+      up[u] = UP[o + u];
+      rh[u] = RH[o + u];
+    }
+    part_solve<P, M>(lo, up, rh, c);
+#pragma unroll
+    for (int u = 0; u < M; ++u) RH[o + u] = rh[u];
+  }
+  __syncthreads();
+  // 4. write back
+  double wsum = 0.0;
+  double pv[M];
+  if (FINAL) {
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      pv[u] = a.psi[po + node(l, min(e, n - 1), i, j, k)];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < M; ++u) {
+    int l, e, i, j, k;
+    elem(u, l, e);
+    if (exists(l, e)) {
+      const int nd = node(l, e, i, j, k);
+      const double x = RH[slot(l, e)];
+      if (FINAL) {
+        a.psi[po + nd] = pv[u] + x;
+        const double r = rnode<K>(g, i), s = snode<K>(g, j);
+        wsum += r * r * s * x * x;
+      } else {
+        R[nd] = x;
+      }
+    }
+  }
+  if (FINAL) {
+    wsum *= g.dr * g.dth * g.dph;
+    __shared__ double sh[4];
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_down_sync(FULL, wsum, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int b = (AX == 2) ? blockIdx.x : blockIdx.y * gridDim.x + blockIdx.x;
+      a.part[(long long)patch * a.maxb + b] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// launch: pick (P, M) with P*M >= n
+// ---------------------------------------------------------------------------------
+template <int Q, int AX, int MODE, int S, int P, int M>
+int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  constexpr int NL = 128 / P;
+  const size_t smem = (size_t)3 * NL * line_pitch<P, (M | 1)>() * sizeof(double);
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_line<Q, AX, MODE, S, P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid;
+  if (AX == 2) {
+    const int nlines = ((K == KR) ? g.nr - 1 : g.nr) * (NTk(g, K) - 2);
+    grid = dim3((nlines + NL - 1) / NL, npatch);
+  } else {
+    grid = dim3((NPk(g, K) - 2 + NL - 1) / NL, AX == 0 ? NTk(g, K) - 2 : (K == KR ? g.nr - 1 : g.nr), npatch);
+  }
+  k_line<Q, AX, MODE, S, P, M><<<grid, 128, smem, st>>>(g, a, ra);
+  return (int)(grid.x * grid.y);
+}
+
+template <int Q, int AX, int MODE, int S>
+int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+#define YY_L(P_, M_) return launch_line<Q, AX, MODE, S, P_, M_>(g, a, ra, npatch, st)
+  if constexpr (AX == 2) {
+    const int n = NPk(g, K) - 2;
+    if (n <= 128) YY_L(32, 4);
+    if (n <= 256) YY_L(32, 8);
+    if (n <= 384) YY_L(32, 12);
+    if (n <= 512) YY_L(32, 16);
+    if (n <= 768) YY_L(32, 24);
+    YY_L(32, 36);                                  // n <= 1152 (checked at create)
+  } else {
+    const int n = (AX == 0) ? ((K == KR) ? g.nr - 1 : g.nr) : NTk(g, K) - 2;
+    if (n <= 16) YY_L(4, 4);
+    if (n <= 32) YY_L(4, 8);
+    if (n <= 64) YY_L(8, 8);
+    if (n <= 96) YY_L(16, 6);
+    if (n <= 128) YY_L(16, 8);
+    if (n <= 256) YY_L(32, 8);
+    if (n <= 384) YY_L(32, 12);
+    YY_L(32, 16);                                  // n <= 512 (checked at create)
+  }
+#undef YY_L
+}
+
+// factor orders (RD28): T r,th,ph; u_r th,ph,r; u_th ph,r,th; u_ph r,th,ph
+constexpr int FIRST_AX[4] = {0, 1, 2, 0};
+constexpr int LAST_AX[4] = {2, 0, 1, 2};
+
+template <int Q, int AX>
+int sweep_axis(const Geo& g, int s, bool first, bool fin, const SweepArgs& a, const ResidArgs* ra, int npatch,
+               cudaStream_t st) {
+  const ResidArgs none{};
+  if constexpr (AX == LAST_AX[Q]) {
+    if (fin) return sweep_line<Q, AX, MODE_FINAL, 1>(g, a, none, npatch, st);
+  }
+  if constexpr (AX == FIRST_AX[Q]) {
+    if (first && ra) {
+      if (Q == QT || s == 1) return sweep_line<Q, AX, MODE_FIRST, 1>(g, a, *ra, npatch, st);
+      if constexpr (Q != QT) return sweep_line<Q, AX, MODE_FIRST, 2>(g, a, *ra, npatch, st);
+    }
+  }
+  if (fin || first) return -1;                     // not a factor position of this quantity
+  return sweep_line<Q, AX, MODE_PLAIN, 1>(g, a, none, npatch, st);
+}
+
+}  // namespace
+
+
+template <int Q>
+int launch_sweep_q(const Geo& g, int ax, int s, bool first, bool fin, const SweepArgs& a, const ResidArgs* ra,
+                   int npatch, cudaStream_t st) {
+  if (ax == 0) return sweep_axis<Q, 0>(g, s, first, fin, a, ra, npatch, st);
+  if (ax == 1) return sweep_axis<Q, 1>(g, s, first, fin, a, ra, npatch, st);
+  return sweep_axis<Q, 2>(g, s, first, fin, a, ra, npatch, st);
+}
+
+// one translation unit per quantity (csrc/build.sh compiles this file with
+// -DYY_LINE_Q=0..3 in parallel)
+#ifdef YY_LINE_Q
+template int launch_sweep_q<YY_LINE_Q>(const Geo&, int, int, bool, bool, const SweepArgs&, const ResidArgs*, int,
+                                       cudaStream_t);
+#endif
+
+}  // namespace yy

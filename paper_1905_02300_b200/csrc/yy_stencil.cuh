@@ -1,0 +1,163 @@
+// yy_stencil.cuh — MAC stencils shared by the per-step kernels (yy_kernels.cu)
+// and the fused residual of the first line sweep (yy_line.cu): 7-point stars
+// with the wall ghost (RD22), sum_d L_{Q,d} (rows of coef<>), divergence pieces
+// and the eq:er residual of one node (sign RD9).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "yy_dev.cuh"
+#include "yy_internal.h"
+
+namespace yy {
+
+// ---------------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------------
+struct Star {   // 7-point star of a field at a node; x = r, y = theta, z = phi
+  double c, xm, xp, ym, yp, zm, zp;
+};
+
+__device__ __forceinline__ Star star_lin(const Star& a, double fa, const Star& b, double fb) {
+  Star s;
+  s.c = fa * a.c + fb * b.c;
+  s.xm = fa * a.xm + fb * b.xm;
+  s.xp = fa * a.xp + fb * b.xp;
+  s.ym = fa * a.ym + fb * b.ym;
+  s.yp = fa * a.yp + fb * b.yp;
+  s.zm = fa * a.zm + fb * b.zm;
+  s.zp = fa * a.zp + fb * b.zp;
+  return s;
+}
+
+// Star of field F (one patch) at (i,j,k).  For r-centred kinds the r
+// neighbours beyond the walls are the ghosts 2 w - psi_0 (reading RD22),
+// W = the field's wall data (2, NT, NP) at the matching time level.
+template <int K>
+__device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict__ F,
+                                          const double* __restrict__ W, int i, int j, int k) {
+  Star s;
+  s.c = F[IX<K>(g, i, j, k)];
+  if (K != KR && i == 0) s.xm = 2.0 * W[(long long)j * NPk(g, K) + k] - s.c;
+  else s.xm = F[IX<K>(g, i - 1, j, k)];
+  if (K != KR && i == g.nr - 1) s.xp = 2.0 * W[wsize(g, K) + (long long)j * NPk(g, K) + k] - s.c;
+  else s.xp = F[IX<K>(g, i + 1, j, k)];
+  s.ym = F[IX<K>(g, i, j - 1, k)];
+  s.yp = F[IX<K>(g, i, j + 1, k)];
+  s.zm = F[IX<K>(g, i, j, k - 1)];
+  s.zp = F[IX<K>(g, i, j, k + 1)];
+  return s;
+}
+
+// sum_d L_{Q,d} applied to a star.
+template <int Q, bool HAT>
+__device__ __forceinline__ double applyL(const Geo& g, const Astar& A, int i, int j, int k, const Star& s) {
+  double am, a0, ap, acc;
+  coef<Q, 0, HAT>(g, A, i, j, k, am, a0, ap);
+  acc = am * s.xm + a0 * s.c + ap * s.xp;
+  coef<Q, 1, HAT>(g, A, i, j, k, am, a0, ap);
+  acc += am * s.ym + a0 * s.c + ap * s.yp;
+  coef<Q, 2, HAT>(g, A, i, j, k, am, a0, ap);
+  acc += am * s.zm + a0 * s.c + ap * s.zp;
+  return acc;
+}
+
+template <int K>
+__device__ __forceinline__ bool solved(const Geo& g, int i, int j, int k) {
+  return i >= i_lo<K>() && i <= i_hi<K>(g) && j >= 1 && j <= NTk(g, K) - 2 && k >= 1 && k <= NPk(g, K) - 2;
+}
+
+// divergence contributions at cell centre (i,j,k) of one patch
+__device__ __forceinline__ double div1(const Geo& g, const double* ur, int i, int j, int k) {
+  return (__ldg(g.rf2 + i + 1) * ur[IX<KR>(g, i + 1, j, k)] - __ldg(g.rf2 + i) * ur[IX<KR>(g, i, j, k)]) *
+         __ldg(g.idv1_c + i);
+}
+__device__ __forceinline__ double div2(const Geo& g, const double* ut, int i, int j, int k) {
+  return (__ldg(g.sf + j + 1) * ut[IX<KT>(g, i, j + 1, k)] - __ldg(g.sf + j) * ut[IX<KT>(g, i, j, k)]) *
+         (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idth);
+}
+__device__ __forceinline__ double div3(const Geo& g, const double* up, int i, int j, int k) {
+  return (up[IX<KP>(g, i, j, k + 1)] - up[IX<KP>(g, i, j, k)]) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
+}
+
+// eq:er residual (sign RD9) at solved node (i,j,k) of patch `patch`:
+//   R = G + tau E_dyn - (I - tau/2 L_split)(psi~ - psi^n)
+// with the Gauss-Seidel dynamic terms E_dyn of SURVEY §8(c) O7/O9 (RD20, RD21,
+// RD18, RD-E1).
+template <int Q, int S>
+__device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int patch, int i, int j, int k) {
+  constexpr int K = kind_of(Q);
+  const long long po = patch * psize(g, K);
+  const long long pc = patch * psize(g, KC);
+  const int node = IX<K>(g, i, j, k);
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+  const double* Wnew = a.wnew ? a.wnew + patch * 2 * wsize(g, K) : nullptr;
+  const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
+  Star x1 = load_star<K>(g, a.it + po, Wnew, i, j, k);
+  Star x0 = load_star<K>(g, a.n + po, Wn, i, j, k);
+  Star X = star_lin(x1, 1.0, x0, -1.0);
+  double E = 0.0;
+  if (Q == QUR) {
+    // buoyancy +Pr Ra T^{n+1/2,(k)} e_r (RD20, RD21)
+    const double* Ti = a.Tit + pc;
+    const double* Tn = a.Tn + pc;
+    const double tb0 = 0.5 * (Ti[IX<KC>(g, i - 1, j, k)] + Tn[IX<KC>(g, i - 1, j, k)]);
+    const double tb1 = 0.5 * (Ti[IX<KC>(g, i, j, k)] + Tn[IX<KC>(g, i, j, k)]);
+    E = g.PrRa * 0.5 * (tb0 + tb1);
+  } else if (Q == QUT) {
+    // c_chi D21 ub_r + nu((2/r^2) d_th ub_r + (2 cos/(r^3 sin)) d_r(r^2 ub_r))  (eq:theta_comp)
+    const long long orr = patch * psize(g, KR);
+    const double *uri = a.urit + orr, *urn = a.urn + orr;
+    auto ub = [&](int ii, int jj) {
+      const long long q = IX<KR>(g, ii, jj, k);
+      return 0.5 * (uri[q] + urn[q]);
+    };
+    const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
+    auto d1 = [&](int jj) { return (f1 * ub(i + 1, jj) - f0 * ub(i, jj)) * iv; };
+    const double ir = __ldg(g.ir_c + i);
+    const double d1a = d1(j - 1), d1b = d1(j);
+    E = g.cchi * (d1b - d1a) * (ir * g.idth);
+    E += g.nu * (2.0 * ir * ir) * 0.5 * ((ub(i, j) - ub(i, j - 1)) + (ub(i + 1, j) - ub(i + 1, j - 1))) * g.idth;
+    E += g.nu * (2.0 * __ldg(g.cot_f + j) * ir) * 0.5 * (d1a + d1b);
+  } else if (Q == QUP) {
+    // c_chi (D31 ub_r + D32 ub_th) + nu((2/(r^2 sin)) d_ph ub_r + (2cos/(r^2 sin^2)) d_ph ub_th)
+    const long long orr = patch * psize(g, KR), ot = patch * psize(g, KT);
+    const double *uri = a.urit + orr, *urn = a.urn + orr, *uti = a.utit + ot, *utn = a.utn + ot;
+    auto ubr = [&](int ii, int kk) {
+      const long long q = IX<KR>(g, ii, j, kk);
+      return 0.5 * (uri[q] + urn[q]);
+    };
+    auto ubt = [&](int jj, int kk) {
+      const long long q = IX<KT>(g, i, jj, kk);
+      return 0.5 * (uti[q] + utn[q]);
+    };
+    const double ir = __ldg(g.ir_c + i), is = __ldg(g.is_c + j), ct = __ldg(g.cot_c + j);
+    const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
+    const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1);
+    const double rsdt = ir * is * g.idth;
+    auto e = [&](int kk) {
+      const double dd1 = (f1 * ubr(i + 1, kk) - f0 * ubr(i, kk)) * iv;
+      const double dd2 = (s1 * ubt(j + 1, kk) - s0 * ubt(j, kk)) * rsdt;
+      return dd1 + dd2;
+    };
+    const double rsdp = ir * is * g.idph;
+    E = g.cchi * (e(k) - e(k - 1)) * rsdp;
+    E += g.nu * (2.0 * ir * rsdp) * 0.5 * ((ubr(i, k) - ubr(i, k - 1)) + (ubr(i + 1, k) - ubr(i + 1, k - 1)));
+    E += g.nu * (2.0 * ct * ir * rsdp) * 0.5 * ((ubt(j, k) - ubt(j, k - 1)) + (ubt(j + 1, k) - ubt(j + 1, k - 1)));
+  }
+  if (S == 2 && Q != QT) {
+    // -1/2 grad(p1^(k) - p1^n)   (RD18)
+    const double *pi_ = a.p1it + pc, *pn = a.p1n + pc;
+    auto dp = [&](int ii, int jj, int kk) {
+      const long long q = IX<KC>(g, ii, jj, kk);
+      return pi_[q] - pn[q];
+    };
+    if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) * g.idr;
+    if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) * (__ldg(g.ir_c + i) * g.idth);
+    if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
+  }
+  const double LX = applyL<Q, true>(g, A, i, j, k, X);
+  return a.G[po + node] + g.tau * E - (X.c - 0.5 * g.tau * LX);
+}
+
+}  // namespace yy

@@ -153,6 +153,34 @@ def test_line_solve_c4_reduced():
         assert np.max(np.abs(got[m] - ref[m])) <= 1e-13 * np.max(np.abs(ref[m])), axis
 
 
+@pytest.mark.parametrize("shape", [(30, 12, 36), (60, 12, 36), (90, 12, 36), (120, 12, 36), (250, 12, 36),
+                                   (300, 12, 36), (5, 60, 180), (5, 100, 300), (4, 200, 600), (4, 300, 900),
+                                   (3, 12, 100), (4, 16, 200), (3, 12, 300), (4, 20, 500), (3, 24, 700),
+                                   (3, 40, 1100)])
+def test_line_solve_every_chunking(shape):
+    """One case per (P chunks, M rows) dispatch branch of the line solver
+    (yy_line.cu), incl. ragged lines (rows past n are identity rows) and the
+    longest supported lines (512 r/theta rows, 1152 phi rows)."""
+    import torch
+    from oracle import ops
+    nr, nt, npp = shape
+    a, rhs = W.c4_inputs(nr, nt, npp)
+    cfg = W.Config("C4", nr, nt, npp, dt=1e-4)
+    sh = _shell(cfg)
+    o = _oracle(cfg)
+    astar = [a["ur"], a["ut"], a["up"]]
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    m = o.g.solved_mask("C")
+    for axis in range(3):
+        x = dev(rhs)
+        sh.line_solve(axis, dev(a["ur"]), dev(a["ut"]), dev(a["up"]), x)
+        torch.cuda.synchronize()
+        got = x.cpu().numpy()
+        ref = o.sweep("T", rhs, axis, ops.coeffs(o.g, o.prm, "T", axis, True, astar))
+        assert np.max(np.abs(got[m] - ref[m])) <= 1e-13 * np.max(np.abs(ref[m])), (shape, axis)
+        assert np.array_equal(got[~m], rhs[~m]), (shape, axis)   # fringe untouched
+
+
 def test_errors_are_reported():
     from paper_1905_02300_b200 import YYError
     cfg = W.small("C1", 4, 12, 28)
