@@ -205,7 +205,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
 
 // Solved-node ranges of a kind (reading RD3): fringe = outermost theta/phi
 // layer; u_r wall faces excluded.
-template <int K> __device__ __forceinline__ int i_lo() { return K == KR ? 1 : 0; }
-template <int K> __device__ __forceinline__ int i_hi(const Geo& g) { return K == KR ? g.nr - 1 : g.nr - 1; }
+template <int K> __host__ __device__ __forceinline__ int i_lo() { return K == KR ? 1 : 0; }
+template <int K> __host__ __device__ __forceinline__ int i_hi(const Geo& g) { return K == KR ? g.nr - 1 : g.nr - 1; }
 
 }  // namespace yy

@@ -12,6 +12,7 @@
 //   K7  k_pres<S>        pressure updates eq:nst_Mass1 / eq:ac2 (RD18)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "yy_dev.cuh"
 #include "yy_internal.h"
@@ -129,15 +130,23 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
 // per thread (resid_at of yy_stencil.cuh).  The step normally fuses it into the
 // first sweep of each quantity (yy_line.cu) when YY_FUSE=1.
 // ---------------------------------------------------------------------------------
-template <int Q, int S>
+template <int Q, int S, int IB>
 __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
+  // thread = one (j, k) column, IB consecutive r-nodes (setup amortised, r-neighbours
+  // of consecutive nodes shared through L1)
   constexpr int K = kind_of(Q);
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y;
-  const int patch = blockIdx.z / NRk(g, K);
-  const int i = blockIdx.z % NRk(g, K);
-  if (k >= NPk(g, K) || !solved<K>(g, i, j, k)) return;
-  a.R[patch * psize(g, K) + IX<K>(g, i, j, k)] = resid_at<Q, S>(g, a, patch, i, j, k);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int j = blockIdx.y + 1;
+  const int nch = (i_hi<K>(g) - i_lo<K>() + IB) / IB;
+  const int patch = blockIdx.z / nch;
+  const int i0 = i_lo<K>() + (blockIdx.z % nch) * IB;
+  if (k > NPk(g, K) - 2) return;
+  double* __restrict__ R = a.R + patch * psize(g, K);
+#pragma unroll
+  for (int u = 0; u < IB; ++u) {
+    const int i = i0 + u;
+    if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S>(g, a, patch, i, j, k);
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -293,11 +302,26 @@ void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st) {
   }
 }
 
+template <int Q, int S, int IB>
+void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  const int nch = (i_hi<K>(g) - i_lo<K>() + IB) / IB;
+  const dim3 grid((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, 2 * nch);
+  k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
+}
+template <int Q, int S>
+void resid_q(const Geo& g, const ResidArgs& a, cudaStream_t st) {
+  static int ib = -1;
+  if (ib < 0) { const char* e = getenv("YY_RESID_IB"); ib = e ? atoi(e) : 4; }
+  if (ib == 1) resid_qb<Q, S, 1>(g, a, st);
+  else resid_qb<Q, S, 4>(g, a, st);
+}
+
 void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t st) {
-  if (q == QT) k_resid<QT, 1><<<pgrid(g, KC, 2), 128, 0, st>>>(g, a);
-  else if (q == QUR) { if (s == 1) k_resid<QUR, 1><<<pgrid(g, KR, 2), 128, 0, st>>>(g, a); else k_resid<QUR, 2><<<pgrid(g, KR, 2), 128, 0, st>>>(g, a); }
-  else if (q == QUT) { if (s == 1) k_resid<QUT, 1><<<pgrid(g, KT, 2), 128, 0, st>>>(g, a); else k_resid<QUT, 2><<<pgrid(g, KT, 2), 128, 0, st>>>(g, a); }
-  else { if (s == 1) k_resid<QUP, 1><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); else k_resid<QUP, 2><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); }
+  if (q == QT) resid_q<QT, 1>(g, a, st);
+  else if (q == QUR) { if (s == 1) resid_q<QUR, 1>(g, a, st); else resid_q<QUR, 2>(g, a, st); }
+  else if (q == QUT) { if (s == 1) resid_q<QUT, 1>(g, a, st); else resid_q<QUT, 2>(g, a, st); }
+  else { if (s == 1) resid_q<QUP, 1>(g, a, st); else resid_q<QUP, 2>(g, a, st); }
 }
 
 int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st) {

@@ -111,6 +111,31 @@ __device__ __forceinline__ void part_solve(double (&lo)[M], double (&up)[M], dou
   rh[M - 1] = gc;
 }
 
+__device__ __forceinline__ void pf_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// L1 prefetch of the a* values coef<Q,AX,true> reads at node (i,j,k) of kind K
+// (the neighbours along the line are the thread's / warp's other elements)
+template <int Q, int AX>
+__device__ __forceinline__ void prefetch_rows(const Geo& g, const Astar& A, int i, int j, int k) {
+  constexpr int K = kind_of(Q);
+  if (AX == 0) {
+    pf_l1(A.ar + IX<KR>(g, i, j, k));
+    if (K == KT) pf_l1(A.ar + IX<KR>(g, i, j - 1, k));
+  } else if (AX == 1) {
+    pf_l1(A.at + IX<KT>(g, i, j, k));
+    if (K == KR) pf_l1(A.at + IX<KT>(g, i - 1, j, k));
+    if (Q == QUT) { pf_l1(A.ar + IX<KR>(g, i, j, k)); pf_l1(A.ar + IX<KR>(g, i + 1, j, k)); }
+  } else {
+    pf_l1(A.ap + IX<KP>(g, i, j, k));
+    if (K == KR) pf_l1(A.ap + IX<KP>(g, i - 1, j, k));
+    if (K == KT) pf_l1(A.ap + IX<KP>(g, i, j - 1, k));
+    if (Q == QUP) {
+      pf_l1(A.ar + IX<KR>(g, i, j, k)); pf_l1(A.ar + IX<KR>(g, i + 1, j, k));
+      pf_l1(A.at + IX<KT>(g, i, j, k)); pf_l1(A.at + IX<KT>(g, i, j + 1, k));
+    }
+  }
+}
+
 // normalised row m (0..n-1) of the factor at node (i,j,k); rv = right-hand side
 template <int Q, int AX>
 __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, int j, int k, int m, int n,
@@ -169,7 +194,6 @@ __global__ void __launch_bounds__(128) k_line(Geo g, SweepArgs a, ResidArgs ra) 
   constexpr int NL = 128 / P;
   constexpr int MP = M | 1;
   constexpr int LP = line_pitch<P, MP>();
-  constexpr int LN = P * M;                // padded line length
   extern __shared__ double sm[];
   double* LO = sm;
   double* UP = LO + NL * LP;
@@ -247,6 +271,16 @@ __global__ void __launch_bounds__(128) k_line(Geo g, SweepArgs a, ResidArgs ra) 
       RH[s] = rh * mk;
     }
   } else {
+    // the transport-velocity rows coef<> reads for these elements go to L1 first
+    // (no registers held), so make_row below finds them there instead of paying a
+    // DRAM round trip per element
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      node(l, min(e, n - 1), i, j, k);
+      prefetch_rows<Q, AX>(g, A, i, j, k);
+    }
     double rv[M];
 #pragma unroll
     for (int u = 0; u < M; ++u) {

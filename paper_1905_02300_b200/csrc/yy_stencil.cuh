@@ -36,16 +36,19 @@ __device__ __forceinline__ Star star_lin(const Star& a, double fa, const Star& b
 template <int K>
 __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict__ F,
                                           const double* __restrict__ W, int i, int j, int k) {
+  // read-only (non-coherent) loads: no kernel that calls this writes F or W
   Star s;
-  s.c = F[IX<K>(g, i, j, k)];
-  if (K != KR && i == 0) s.xm = 2.0 * W[(long long)j * NPk(g, K) + k] - s.c;
-  else s.xm = F[IX<K>(g, i - 1, j, k)];
-  if (K != KR && i == g.nr - 1) s.xp = 2.0 * W[wsize(g, K) + (long long)j * NPk(g, K) + k] - s.c;
-  else s.xp = F[IX<K>(g, i + 1, j, k)];
-  s.ym = F[IX<K>(g, i, j - 1, k)];
-  s.yp = F[IX<K>(g, i, j + 1, k)];
-  s.zm = F[IX<K>(g, i, j, k - 1)];
-  s.zp = F[IX<K>(g, i, j, k + 1)];
+  const int nd = IX<K>(g, i, j, k);
+  const int sr = NTk(g, K) * NPk(g, K), st = NPk(g, K);
+  s.c = __ldg(F + nd);
+  if (K != KR && i == 0) s.xm = 2.0 * __ldg(W + j * NPk(g, K) + k) - s.c;
+  else s.xm = __ldg(F + nd - sr);
+  if (K != KR && i == g.nr - 1) s.xp = 2.0 * __ldg(W + wsize(g, K) + j * NPk(g, K) + k) - s.c;
+  else s.xp = __ldg(F + nd + sr);
+  s.ym = __ldg(F + nd - st);
+  s.yp = __ldg(F + nd + st);
+  s.zm = __ldg(F + nd - 1);
+  s.zp = __ldg(F + nd + 1);
   return s;
 }
 
@@ -101,8 +104,8 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     // buoyancy +Pr Ra T^{n+1/2,(k)} e_r (RD20, RD21)
     const double* Ti = a.Tit + pc;
     const double* Tn = a.Tn + pc;
-    const double tb0 = 0.5 * (Ti[IX<KC>(g, i - 1, j, k)] + Tn[IX<KC>(g, i - 1, j, k)]);
-    const double tb1 = 0.5 * (Ti[IX<KC>(g, i, j, k)] + Tn[IX<KC>(g, i, j, k)]);
+    const double tb0 = 0.5 * (__ldg(Ti + IX<KC>(g, i - 1, j, k)) + __ldg(Tn + IX<KC>(g, i - 1, j, k)));
+    const double tb1 = 0.5 * (__ldg(Ti + IX<KC>(g, i, j, k)) + __ldg(Tn + IX<KC>(g, i, j, k)));
     E = g.PrRa * 0.5 * (tb0 + tb1);
   } else if (Q == QUT) {
     // c_chi D21 ub_r + nu((2/r^2) d_th ub_r + (2 cos/(r^3 sin)) d_r(r^2 ub_r))  (eq:theta_comp)
@@ -110,7 +113,7 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     const double *uri = a.urit + orr, *urn = a.urn + orr;
     auto ub = [&](int ii, int jj) {
       const long long q = IX<KR>(g, ii, jj, k);
-      return 0.5 * (uri[q] + urn[q]);
+      return 0.5 * (__ldg(uri + q) + __ldg(urn + q));
     };
     const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
     auto d1 = [&](int jj) { return (f1 * ub(i + 1, jj) - f0 * ub(i, jj)) * iv; };
@@ -125,11 +128,11 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     const double *uri = a.urit + orr, *urn = a.urn + orr, *uti = a.utit + ot, *utn = a.utn + ot;
     auto ubr = [&](int ii, int kk) {
       const long long q = IX<KR>(g, ii, j, kk);
-      return 0.5 * (uri[q] + urn[q]);
+      return 0.5 * (__ldg(uri + q) + __ldg(urn + q));
     };
     auto ubt = [&](int jj, int kk) {
       const long long q = IX<KT>(g, i, jj, kk);
-      return 0.5 * (uti[q] + utn[q]);
+      return 0.5 * (__ldg(uti + q) + __ldg(utn + q));
     };
     const double ir = __ldg(g.ir_c + i), is = __ldg(g.is_c + j), ct = __ldg(g.cot_c + j);
     const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
@@ -150,14 +153,14 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     const double *pi_ = a.p1it + pc, *pn = a.p1n + pc;
     auto dp = [&](int ii, int jj, int kk) {
       const long long q = IX<KC>(g, ii, jj, kk);
-      return pi_[q] - pn[q];
+      return __ldg(pi_ + q) - __ldg(pn + q);
     };
     if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) * g.idr;
     if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) * (__ldg(g.ir_c + i) * g.idth);
     if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
   }
   const double LX = applyL<Q, true>(g, A, i, j, k, X);
-  return a.G[po + node] + g.tau * E - (X.c - 0.5 * g.tau * LX);
+  return __ldg(a.G + po + node) + g.tau * E - (X.c - 0.5 * g.tau * LX);
 }
 
 }  // namespace yy
