@@ -63,10 +63,19 @@ __host__ __device__ __forceinline__ long long wsize(const Geo& g, int K) {   // 
 }
 // Offset of node (i,j,k) inside ONE patch's array of kind K.  32-bit: the
 // largest per-patch array (C4, 257x385x1153) has 1.1e8 < 2^31 elements.
+// All kinds are written through the cell-centre index c = (i nt + j) np + k so
+// that the indices of one node in arrays of different kinds share it (CSE):
+//   IX<KT> = (i (nt+1) + j) np + k = c + i np,  IX<KP> = (i nt + j)(np+1) + k = c + i nt + j.
 template <int K>
 __device__ __forceinline__ int IX(const Geo& g, int i, int j, int k) {
-  return (i * NTk(g, K) + j) * NPk(g, K) + k;
+  const int c = (i * g.nt + j) * g.np + k;
+  if (K == KT) return c + i * g.np;
+  if (K == KP) return c + i * g.nt + j;
+  return c;
 }
+// index strides of kind K along r (SR) and theta (ST); phi stride is 1
+template <int K> __host__ __device__ __forceinline__ int SR(const Geo& g) { return NTk(g, K) * NPk(g, K); }
+template <int K> __host__ __device__ __forceinline__ int ST(const Geo& g) { return NPk(g, K); }
 
 // Transport velocity a* = u2^{*,n+1/2} (RD8), one patch.
 struct Astar {
@@ -79,36 +88,30 @@ struct Astar {
 // staggerings differ; SURVEY Appendix A "Advection").
 template <int K>
 __device__ __forceinline__ double abar_r(const Geo& g, const Astar& A, int i, int j, int k) {
-  const double* a = A.ar;
-  if (K == KR) return __ldg(a + IX<KR>(g, i, j, k));
-  if (K == KC) return 0.5 * (__ldg(a + IX<KR>(g, i, j, k)) + __ldg(a + IX<KR>(g, i + 1, j, k)));
-  if (K == KT)
-    return 0.25 * (__ldg(a + IX<KR>(g, i, j - 1, k)) + __ldg(a + IX<KR>(g, i + 1, j - 1, k)) +
-                   __ldg(a + IX<KR>(g, i, j, k)) + __ldg(a + IX<KR>(g, i + 1, j, k)));
-  return 0.25 * (__ldg(a + IX<KR>(g, i, j, k - 1)) + __ldg(a + IX<KR>(g, i + 1, j, k - 1)) +
-                 __ldg(a + IX<KR>(g, i, j, k)) + __ldg(a + IX<KR>(g, i + 1, j, k)));
+  const double* a = A.ar + IX<KR>(g, i, j, k);
+  const int sr = SR<KR>(g), st = ST<KR>(g);
+  if (K == KR) return __ldg(a);
+  if (K == KC) return 0.5 * (__ldg(a) + __ldg(a + sr));
+  if (K == KT) return 0.25 * (__ldg(a - st) + __ldg(a + sr - st) + __ldg(a) + __ldg(a + sr));
+  return 0.25 * (__ldg(a - 1) + __ldg(a + sr - 1) + __ldg(a) + __ldg(a + sr));
 }
 template <int K>
 __device__ __forceinline__ double abar_t(const Geo& g, const Astar& A, int i, int j, int k) {
-  const double* a = A.at;
-  if (K == KT) return __ldg(a + IX<KT>(g, i, j, k));
-  if (K == KC) return 0.5 * (__ldg(a + IX<KT>(g, i, j, k)) + __ldg(a + IX<KT>(g, i, j + 1, k)));
-  if (K == KR)
-    return 0.25 * (__ldg(a + IX<KT>(g, i - 1, j, k)) + __ldg(a + IX<KT>(g, i - 1, j + 1, k)) +
-                   __ldg(a + IX<KT>(g, i, j, k)) + __ldg(a + IX<KT>(g, i, j + 1, k)));
-  return 0.25 * (__ldg(a + IX<KT>(g, i, j, k - 1)) + __ldg(a + IX<KT>(g, i, j + 1, k - 1)) +
-                 __ldg(a + IX<KT>(g, i, j, k)) + __ldg(a + IX<KT>(g, i, j + 1, k)));
+  const double* a = A.at + IX<KT>(g, i, j, k);
+  const int sr = SR<KT>(g), st = ST<KT>(g);
+  if (K == KT) return __ldg(a);
+  if (K == KC) return 0.5 * (__ldg(a) + __ldg(a + st));
+  if (K == KR) return 0.25 * (__ldg(a - sr) + __ldg(a - sr + st) + __ldg(a) + __ldg(a + st));
+  return 0.25 * (__ldg(a - 1) + __ldg(a + st - 1) + __ldg(a) + __ldg(a + st));
 }
 template <int K>
 __device__ __forceinline__ double abar_p(const Geo& g, const Astar& A, int i, int j, int k) {
-  const double* a = A.ap;
-  if (K == KP) return __ldg(a + IX<KP>(g, i, j, k));
-  if (K == KC) return 0.5 * (__ldg(a + IX<KP>(g, i, j, k)) + __ldg(a + IX<KP>(g, i, j, k + 1)));
-  if (K == KR)
-    return 0.25 * (__ldg(a + IX<KP>(g, i - 1, j, k)) + __ldg(a + IX<KP>(g, i - 1, j, k + 1)) +
-                   __ldg(a + IX<KP>(g, i, j, k)) + __ldg(a + IX<KP>(g, i, j, k + 1)));
-  return 0.25 * (__ldg(a + IX<KP>(g, i, j - 1, k)) + __ldg(a + IX<KP>(g, i, j - 1, k + 1)) +
-                 __ldg(a + IX<KP>(g, i, j, k)) + __ldg(a + IX<KP>(g, i, j, k + 1)));
+  const double* a = A.ap + IX<KP>(g, i, j, k);
+  const int sr = SR<KP>(g), st = ST<KP>(g);
+  if (K == KP) return __ldg(a);
+  if (K == KC) return 0.5 * (__ldg(a) + __ldg(a + 1));
+  if (K == KR) return 0.25 * (__ldg(a - sr) + __ldg(a - sr + 1) + __ldg(a) + __ldg(a + 1));
+  return 0.25 * (__ldg(a - st) + __ldg(a - st + 1) + __ldg(a) + __ldg(a + 1));
 }
 
 // Node coordinates and 1-D factors at the nodes of kind K.

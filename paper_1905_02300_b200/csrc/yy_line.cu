@@ -42,6 +42,7 @@ constexpr unsigned FULL = 0xffffffffu;
 // thread's chunk c (0..P-1) of its line.  On exit rh[t] = x_t.
 template <int P, int M>
 __device__ __forceinline__ void part_solve(double (&lo)[M], double (&up)[M], double (&rh)[M], int c) {
+  (void)c;
   static_assert(M >= 2, "chunk of at least two rows");
   // forward over the interior rows 0..M-2:  x_t + c'_t x_{t+1} = y'_t + v'_t g_{c-1}
   double cp = 0.0, yp = 0.0, vp = 0.0;
@@ -87,21 +88,24 @@ __device__ __forceinline__ void part_solve(double (&lo)[M], double (&up)[M], dou
   double B = ae * up[M - 2] + 1.0 + ce * V0n;
   double C = ce * W0n;
   double D = rh[M - 1] - ae * rh[M - 2] - ce * Y0n;
+  // PCR: equation c reads A g_{c-s} + B g_c + C g_{c+s} = D.  A = 0 for c < s and
+  // C = 0 for c + s >= P hold at every step (A_0 = 0: chunk 0 starts the line;
+  // C_{P-1} = 0: the line ends in chunk P-1), so the out-of-segment partners a
+  // width-P shuffle returns (the lane itself) are multiplied by zero: no selects.
+  // The partners' reciprocal pivots are shuffled instead of their B.
 #pragma unroll
   for (int s = 1; s < P; s <<= 1) {
-    const double Am = __shfl_up_sync(FULL, A, s, P), Bm = __shfl_up_sync(FULL, B, s, P);
+    const double iB = frcp(B);
+    const double Am = __shfl_up_sync(FULL, A, s, P), iBm = __shfl_up_sync(FULL, iB, s, P);
     const double Cm = __shfl_up_sync(FULL, C, s, P), Dm = __shfl_up_sync(FULL, D, s, P);
-    const double Ap = __shfl_down_sync(FULL, A, s, P), Bp = __shfl_down_sync(FULL, B, s, P);
+    const double Ap = __shfl_down_sync(FULL, A, s, P), iBp = __shfl_down_sync(FULL, iB, s, P);
     const double Cp = __shfl_down_sync(FULL, C, s, P), Dp = __shfl_down_sync(FULL, D, s, P);
-    const bool hm = c >= s, hp = c + s < P;
-    const double al = hm ? -A * frcp(Bm) : 0.0;
-    const double ga = hp ? -C * frcp(Bp) : 0.0;
-    const double nA = hm ? al * Am : 0.0;
-    const double nC = hp ? ga * Cp : 0.0;
-    B = B + (hm ? al * Cm : 0.0) + (hp ? ga * Ap : 0.0);
-    D = D + (hm ? al * Dm : 0.0) + (hp ? ga * Dp : 0.0);
-    A = nA;
-    C = nC;
+    const double al = -A * iBm;
+    const double ga = -C * iBp;
+    B = B + al * Cm + ga * Ap;
+    D = D + al * Dm + ga * Dp;
+    A = al * Am;
+    C = ga * Cp;
   }
   const double gc = D * frcp(B);
   const double gp = __shfl_up_sync(FULL, gc, 1, P);
