@@ -12,6 +12,7 @@
 //   K7  k_pres<S>        pressure updates eq:nst_Mass1 / eq:ac2 (RD18)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "yy_dev.cuh"
@@ -309,11 +310,18 @@ void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   const dim3 grid((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, 2 * nch);
   k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
 }
+// r-nodes per thread of the residual, per quantity (measured on B200, C3);
+// YY_RESID_IB=<T>,<ur>,<ut>,<up> overrides (tuning)
 template <int Q, int S>
 void resid_q(const Geo& g, const ResidArgs& a, cudaStream_t st) {
-  static int ib = -1;
-  if (ib < 0) { const char* e = getenv("YY_RESID_IB"); ib = e ? atoi(e) : 4; }
-  if (ib == 1) resid_qb<Q, S, 1>(g, a, st);
+  static int ib[4] = {-1, -1, -1, -1};
+  if (ib[0] < 0) {
+    const int def[4] = {4, 2, 2, 2};
+    for (int q = 0; q < 4; ++q) ib[q] = def[q];
+    if (const char* e = getenv("YY_RESID_IB")) sscanf(e, "%d,%d,%d,%d", &ib[0], &ib[1], &ib[2], &ib[3]);
+  }
+  if (ib[Q] == 1) resid_qb<Q, S, 1>(g, a, st);
+  else if (ib[Q] == 2) resid_qb<Q, S, 2>(g, a, st);
   else resid_qb<Q, S, 4>(g, a, st);
 }
 

@@ -1,5 +1,5 @@
 # quick experiment: parity tests (PYTEST_K selects; ALL runs everything), short benches
-# under each env setting in $VARIANTS ("name:VAR=val,VAR=val ..."), optional ncu of $NCU_K
+# under each env setting in $VARIANTS ("name:VAR=val+VAR=val ..."), optional ncu of $NCU_K
 mkdir -p gpurun_out
 : > gpurun_out/rc.txt
 if [ -n "${PYTEST_K:-}" ]; then
@@ -9,7 +9,7 @@ if [ -n "${PYTEST_K:-}" ]; then
 fi
 for v in ${VARIANTS:-base:}; do
   name=${v%%:*}; envs=${v#*:}
-  env ${envs//,/ } timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$name.log 2>&1
+  env ${envs//+/ } timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$name.log 2>&1
   echo "bench $name rc $?" >> gpurun_out/rc.txt
 done
 if [ -n "${NCU_K:-}" ]; then
