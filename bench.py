@@ -212,13 +212,15 @@ def run_yy(args):
     from paper_1905_02300_b200 import Shell
 
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 2:
         if rank == 0:
             emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                  "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                  "dtype": "f64", "data": "synthetic", "config": {"workload": "C5"},
-                  "error": "multi-GPU layout (Yin/Yang x radial slabs, NCCL) not built yet; N=1 only"})
+                  "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                  "dtype": "f64", "data": "synthetic", "config": {"workload": args.workload},
+                  "error": "radial slabs (4/8 GPUs, partitioned r-solve) not built; N=1 and N=2 (one patch per GPU) are"})
         return 0
+    if world == 2:
+        return run_yy_dist(args, rank, world, local)
     torch.cuda.set_device(local)
     cfg = W.config(args.workload)
     wl = W.make_workload(cfg)
@@ -345,6 +347,64 @@ def run_yy(args):
     }
     emit(out)
     sh.close()
+    return 0
+
+
+def run_yy_dist(args, rank, world, local):
+    """N = 2: one patch per GPU (yy_create_dist over NCCL).  The workload is the
+    N = 1 one, so total work is fixed: "scaling": "strong"."""
+    import torch
+    import torch.distributed as td
+
+    import workloads as W
+    from paper_1905_02300_b200 import Shell, dist
+
+    torch.cuda.set_device(local)
+    td.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = dist.share_unique_id(rank, device=torch.device("cuda", local))
+    cfg = W.config(args.workload)
+    wl = W.make_workload(cfg)
+    stream = torch.cuda.Stream()
+    sh = Shell.dist(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, world, rank, uid, local,
+                    stream=stream.cuda_stream)
+    sh.load_workload(wl)
+    W_ = max(3, args.warmup)
+    for _ in range(W_):
+        sh.step(1, cfg.tol)
+    torch.cuda.synchronize()
+    td.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    td.barrier()
+    ev0.record(stream)
+    sh.step(args.steps, cfg.tol)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    td.barrier()
+    clocks = clk.stop()
+    ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+    td.all_reduce(ms, op=td.ReduceOp.MAX)
+    ms = float(ms.item())
+    Ks = [k for k, _ in sh.stats()[-args.steps:]]
+    forced = len(wl["patches"][0]["sources"]) > 0
+    model_bytes = sum(step_model_bytes(cfg, k, forced) for k in Ks)
+    if rank == 0:
+        emit({"metric": METRIC, "value": 2 * cfg.cells * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+              "steps": args.steps, "warmup": W_, "ms_per_step": ms / args.steps, "higher_is_better": True,
+              "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+              "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
+                         "parallelism": "one patch per GPU (Yin rank 0, Yang rank 1), NCCL fringe + norm swap",
+                         "schwarz_iters_per_step": Ks,
+                         "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
+                                           "frac_of_8TBs_per_gpu": model_bytes / (world * HBM_NOMINAL_GBS * 1e9)
+                                           / (ms / 1e3)}},
+              "clocks": clocks, "timing": "CUDA events on each rank's stream, max over ranks"})
+    sh.close()
+    td.destroy_process_group()
     return 0
 
 

@@ -84,6 +84,21 @@ typedef struct {
 yy_status yy_create(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
                     yy_ctx** out);
 
+/* Multi-GPU: one process per GPU, one context per process.
+ * world = 2: rank r holds patch r (Yin on rank 0, Yang on rank 1) on CUDA device
+ * `device`; every Schwarz iteration the donor rank evaluates the partner's fringe
+ * from its own patch (Alg. 1 steps 1/3/7) and the two ranks swap
+ * them, and the per-(quantity, patch) norms (RD24), over NCCL point-to-point on
+ * the context's stream.  world = 1, rank 0 is yy_create on `device`.  Radial
+ * slabs (world 4, 8) are not built: YY_EINVAL.  nccl_id: 128 bytes from
+ * yy_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
+ * Collective semantics: every rank calls the same sequence of yy_step.  NCCL is
+ * resolved at run time (libnccl.so.2); missing -> YY_ENCCL.  set/get/wall/source
+ * calls accept only the rank's own patch. */
+yy_status yy_create_dist(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
+                         int32_t world, int32_t rank, const void* nccl_id, int32_t device, yy_ctx** out);
+yy_status yy_nccl_unique_id(void* out128);
+
 /* Set one patch's state.  level 0 = t^n, 1 = t^{n-1} (p ignored).  system
  * 0 = both bootstrapped systems (u1 = u2, p1 = p2; eq:ac1/eq:ac2), 1 or 2 =
  * that system only.  T is shared by both systems. */

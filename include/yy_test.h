@@ -28,6 +28,14 @@ yy_status yy_debug_get(yy_ctx* ctx, const char* name, int32_t patch, double* hos
 yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar, const double* d_at,
                         const double* d_ap, double* d_x);
 
+/* Two one-patch contexts in this process on the current device (out2[0] holds
+ * Yin, out2[1] Yang) that exchange fringe values and norms by device copies on
+ * one shared stream: the data path of yy_create_dist (donor-side evaluation,
+ * transfer, target write, fixed-order norm merge) without NCCL, so one GPU can
+ * check it against the oracle.  yy_step on either context advances both. */
+yy_status yy_create_pair(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
+                         yy_ctx** out2);
+
 #ifdef __cplusplus
 }
 #endif

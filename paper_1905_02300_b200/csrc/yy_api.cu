@@ -2,6 +2,8 @@
 // Yin<->Yang stencil construction, and the per-step launch sequence
 // (SURVEY.md §3 (ii)).  Device work is entirely in yy_kernels.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
@@ -45,6 +47,18 @@ struct yy_ctx {
   double R1 = 1, R2 = 2, Pr = 1, Ra = 0, dt = 1e-3, chi = 1.0;
   int max_iters = 100, fixed_iters = 0;
   bool fuse = false;           // residual fused into the first sweep (YY_FUSE=1; measured slower on C3 so far)
+  // distribution: npatch = g.npatch local patches, global id of
+  // local patch 0 = patch0.  mode 0: both patches here; 1: loopback pair (two
+  // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
+  int patch0 = 0;
+  int mode = 0;
+  yy_ctx* peer = nullptr;      // loopback partner
+  int world = 1, rank = 0;
+  void* nccl = nullptr;        // ncclComm_t
+  double* fr_send = nullptr;   // fringe values this patch donates to the partner
+  double* fr_recv = nullptr;   // fringe values received for this patch
+  long long fr_n = 0;
+  double* peer_red = nullptr;  // the partner's per-(slot, patch) sums
   double t = 0.0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -320,6 +334,8 @@ yy_status check_args(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system) 
   if (!ctx) return YY_EINVAL;
   if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
   if (patch < 0 || patch > 1) return fail(ctx, YY_EINVAL, "patch must be 0 (Yin) or 1 (Yang)");
+  if (patch < ctx->patch0 || patch >= ctx->patch0 + ctx->g.npatch)
+    return fail(ctx, YY_EINVAL, "this context does not hold that patch");
   if (level < 0 || level > 1) return fail(ctx, YY_EINVAL, "level must be 0 (t^n) or 1 (t^{n-1})");
   if (system < 0 || system > 2) return fail(ctx, YY_EINVAL, "system must be 0, 1 or 2");
   return YY_OK;
@@ -329,8 +345,8 @@ yy_status check_args(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system) 
 yy_status eval_walls(yy_ctx* ctx, int L, double t) {
   const Geo& g = ctx->g;
   for (int f = 0; f < NW; ++f) {
-    const long long ws = 2 * wsize(g, WKIND[f]);
-    for (int p = 0; p < 2; ++p) {
+    const long long ws = 2 * wsize(g, WKIND[f]);   // inner + outer wall of one patch
+    for (int p = 0; p < g.npatch; ++p) {
       LinIn in{};
       int nin = 0;
       for (int m = 0; m < ctx->nw[p]; ++m)
@@ -362,7 +378,7 @@ StaticArgs static_args(yy_ctx* ctx, int q, double tsrc) {
   a.upn[0] = ctx->n[FUP1]; a.upn[1] = ctx->n[FUP2];
   a.upm[0] = ctx->m[FUP1]; a.upm[1] = ctx->m[FUP2];
   const int sf = (q == QT) ? 0 : q;    // source field index: T, ur, ut, up
-  for (int p = 0; p < 2; ++p) {
+  for (int p = 0; p < ctx->g.npatch; ++p) {
     int k = 0;
     for (int m = 0; m < ctx->ns[p]; ++m)
       if (ctx->sterm[p][m][sf]) {
@@ -412,17 +428,19 @@ yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
     // fused first sweep: class "sweep_<q>_<ax>+resid_<q><s>"
     ProfScope ps(ctx, kname(std::string("sweep_") + QNAME[q] + "_" + AXNAME[ORDER[q][a]] + (fin ? "_fin" : "") +
                             (first ? "+" + rname : "")), 1);
-    const int nb = launch_sweep(g, q, ORDER[q][a], s, first, fin, w, first ? &r : nullptr, 2, ctx->st);
+    const int nb = launch_sweep(g, q, ORDER[q][a], s, first, fin, w, first ? &r : nullptr, g.npatch, ctx->st);
     if (nb < 0) return fail(ctx, YY_ESTATE, "internal: no sweep kernel for this factor");
     if (fin) nblk[slot] = nb;
   }
   return YY_OK;
 }
 
-yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
+// O2-O4 and the walls of one step (per context)
+yy_status step_begin(yy_ctx* ctx) {
   const Geo& g = ctx->g;
   const double tau = ctx->dt, t = ctx->t;
   cudaStream_t st = ctx->st;
+  const int NPT = g.npatch;
   // wall data at t_{n-1}, t_n, t_{n+1}
   for (int L = 0; L < 3; ++L) TRY(eval_walls(ctx, L, t + (L - 1) * tau));
   // O2: a* = 1.5 u2^n - 0.5 u2^{n-1}
@@ -431,7 +449,7 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
     in.p[0] = ctx->n[FUR2 + c]; in.c[0] = 1.5;
     in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
     ProfScope ps(ctx, "astar", 1);
-    launch_lincomb(ctx->astar[c], 2 * fsize(ctx, FUR2 + c), in, 2, st);
+    launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
   }
   // O3: static right-hand sides
   for (int q = 0; q < 4; ++q) {
@@ -442,64 +460,158 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
   // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
   for (int f = 0; f < NF; ++f) {
     ProfScope ps(ctx, "copy_iterate", 0);
-    CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], 2 * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], NPT * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   const long long plane = (long long)g.nt * g.np;
   for (int f : {FUR1, FUR2})
-    for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < NPT; ++p)
       for (int w = 0; w < 2; ++w)
         CK(cudaMemcpyAsync(ctx->it[f] + p * fsize(ctx, f) + (w ? g.nr * plane : 0),
                            ctx->wl[2][WUR] + (p * 2 + w) * plane, plane * sizeof(double),
                            cudaMemcpyDeviceToDevice, st));
+  return YY_OK;
+}
+
+InterpArgs interp_args(yy_ctx* ctx) {
   InterpArgs ia{};
   ia.cc[0] = ctx->it[FT]; ia.cc[1] = ctx->it[FP1]; ia.cc[2] = ctx->it[FP2];
   ia.cc[3] = ctx->it[FUR1]; ia.cc[4] = ctx->it[FUR2];
   ia.ut[0] = ctx->it[FUT1]; ia.ut[1] = ctx->it[FUT2];
   ia.up[0] = ctx->it[FUP1]; ia.up[1] = ctx->it[FUP2];
   ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
-  const int kmax = ctx->fixed_iters > 0 ? ctx->fixed_iters : ctx->max_iters;
-  int k = 0;
-  double rho = INFINITY;
+  return ia;
+}
+
+// O6-O9 of one Schwarz iteration and the local per-(slot, patch) norms (per context)
+yy_status iter_solve(yy_ctx* ctx) {
+  const Geo& g = ctx->g;
+  cudaStream_t st = ctx->st;
   ReduceArgs ra{};
   ra.maxb = ctx->maxb;
-  while (k < kmax) {
-    ++k;
-    {
-      ProfScope ps(ctx, "interp", 3);
-      launch_interp(g, ia, st);                            // O5
-    }
-    TRY(solve_quantity(ctx, QT, 1, 0, ra.nblk));           // O6
-    for (int s = 1; s <= 2; ++s) {                         // O7 / O9
-      const int base = (s == 1) ? 1 : 5;
-      TRY(solve_quantity(ctx, QUR, s, base + 0, ra.nblk));
-      TRY(solve_quantity(ctx, QUT, s, base + 1, ra.nblk));
-      TRY(solve_quantity(ctx, QUP, s, base + 2, ra.nblk));
-      PresArgs pa{};
-      const int o = (s == 2) ? 3 : 0;
-      pa.urit = ctx->it[FUR1 + o]; pa.urn = ctx->n[FUR1 + o];
-      pa.utit = ctx->it[FUT1 + o]; pa.utn = ctx->n[FUT1 + o];
-      pa.upit = ctx->it[FUP1 + o]; pa.upn = ctx->n[FUP1 + o];
-      pa.pn = ctx->n[s == 1 ? FP1 : FP2];
-      pa.p1it = ctx->it[FP1]; pa.p1n = ctx->n[FP1];
-      pa.pit = ctx->it[s == 1 ? FP1 : FP2];
-      pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
-      pa.maxb = ctx->maxb;
-      ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
-      ra.nblk[base + 3] = launch_pres(g, s, pa, st);
-    }
-    {
-      ProfScope ps(ctx, "reduce", 2);
-      launch_reduce(ctx->part, ra, ctx->red, st);          // O10
-    }
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (ctx->prof_on) prof_collect(ctx);
-    rho = ctx->red_host[0];
-    if (ctx->red_host[1] != 0.0) return fail(ctx, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
-    if (ctx->fixed_iters <= 0 && rho < tol) break;
+  ra.npatch = g.npatch;
+  ra.patch0 = ctx->patch0;
+  TRY(solve_quantity(ctx, QT, 1, 0, ra.nblk));           // O6
+  for (int s = 1; s <= 2; ++s) {                         // O7 / O9
+    const int base = (s == 1) ? 1 : 5;
+    TRY(solve_quantity(ctx, QUR, s, base + 0, ra.nblk));
+    TRY(solve_quantity(ctx, QUT, s, base + 1, ra.nblk));
+    TRY(solve_quantity(ctx, QUP, s, base + 2, ra.nblk));
+    PresArgs pa{};
+    const int o = (s == 2) ? 3 : 0;
+    pa.urit = ctx->it[FUR1 + o]; pa.urn = ctx->n[FUR1 + o];
+    pa.utit = ctx->it[FUT1 + o]; pa.utn = ctx->n[FUT1 + o];
+    pa.upit = ctx->it[FUP1 + o]; pa.upn = ctx->n[FUP1 + o];
+    pa.pn = ctx->n[s == 1 ? FP1 : FP2];
+    pa.p1it = ctx->it[FP1]; pa.p1n = ctx->n[FP1];
+    pa.pit = ctx->it[s == 1 ? FP1 : FP2];
+    pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
+    pa.maxb = ctx->maxb;
+    ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
+    ra.nblk[base + 3] = launch_pres(g, s, pa, st);
   }
-  // O11: rotate levels
+  ProfScope ps(ctx, "reduce", 1);
+  launch_reduce_slots(ctx->part, ra, ctx->red, st);      // O10, local patches
+  return YY_OK;
+}
+
+// ---- transports between the contexts of a group --------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// NCCL is resolved at run time (the process's already-loaded libnccl, e.g.
+// torch's, else libnccl.so.2), so libyy.so itself does not depend on it.
+NcclApi& nccl_api() {
+  static NcclApi a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return a;
+#define YY_SYM(f, n) a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, n))
+  YY_SYM(GetUniqueId, "ncclGetUniqueId");
+  YY_SYM(CommInitRank, "ncclCommInitRank");
+  YY_SYM(CommDestroy, "ncclCommDestroy");
+  YY_SYM(Send, "ncclSend");
+  YY_SYM(Recv, "ncclRecv");
+  YY_SYM(GroupStart, "ncclGroupStart");
+  YY_SYM(GroupEnd, "ncclGroupEnd");
+  YY_SYM(GetErrorString, "ncclGetErrorString");
+#undef YY_SYM
+  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart && a.GroupEnd &&
+         a.GetErrorString;
+  return a;
+}
+
+#define NK(call)                                                                            \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess) return fail(ctx, YY_ENCCL, std::string(#call ": ") + nccl_api().GetErrorString(r_)); \
+  } while (0)
+
+// exchange `count` doubles: each context's src goes to its partner's dst
+yy_status swap_with_partner(std::vector<yy_ctx*>& cs, double* yy_ctx::*src, double* yy_ctx::*dst, long long count) {
+  for (yy_ctx* ctx : cs) {
+    if (ctx->mode == 1) {
+      CK(cudaMemcpyAsync(ctx->peer->*dst, ctx->*src, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+    } else if (ctx->mode == 2) {
+      NcclApi& N = nccl_api();
+      ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+      const int partner = 1 - ctx->rank;
+      NK(N.GroupStart());
+      NK(N.Send(ctx->*src, (size_t)count, ncclFloat64, partner, comm, ctx->st));
+      NK(N.Recv(ctx->*dst, (size_t)count, ncclFloat64, partner, comm, ctx->st));
+      NK(N.GroupEnd());
+    }
+  }
+  return YY_OK;
+}
+
+// O5: fringe of every patch from the other patch's iterate k-1
+yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
+  if (cs.size() == 1 && cs[0]->mode == 0) {
+    yy_ctx* ctx = cs[0];
+    ProfScope ps(ctx, "interp", 3);
+    launch_interp(ctx->g, interp_args(ctx), ctx->st);
+    return YY_OK;
+  }
+  for (yy_ctx* ctx : cs) {                                // donor side: the partner's fringe
+    ProfScope ps(ctx, "fringe_pack", 3);
+    launch_fringe_pack(ctx->g, interp_args(ctx), ctx->fr_send, ctx->st);
+  }
+  TRY(swap_with_partner(cs, &yy_ctx::fr_send, &yy_ctx::fr_recv, cs[0]->fr_n));
+  for (yy_ctx* ctx : cs) {
+    ProfScope ps(ctx, "fringe_unpack", 3);
+    launch_fringe_unpack(ctx->g, interp_args(ctx), ctx->fr_recv, ctx->st);
+  }
+  return YY_OK;
+}
+
+// O10: rho_k from the sums of all patches (fixed order, identical on every context)
+yy_status reduce_group(std::vector<yy_ctx*>& cs) {
+  if (!(cs.size() == 1 && cs[0]->mode == 0)) {
+    TRY(swap_with_partner(cs, &yy_ctx::red, &yy_ctx::peer_red, 2 + 2 * NSLOT));
+    for (yy_ctx* ctx : cs) launch_merge_sums(ctx->red, ctx->peer_red, 1 - ctx->patch0, ctx->st);
+  }
+  for (yy_ctx* ctx : cs) {
+    ProfScope ps(ctx, "reduce", 1);
+    launch_reduce_final(ctx->red, ctx->st);
+  }
+  return YY_OK;
+}
+
+// O11: rotate levels, advance t (per context)
+void step_end(yy_ctx* ctx) {
   for (int f = 0; f < NF; ++f) {
     if (f == FP1 || f == FP2) {
       std::swap(ctx->n[f], ctx->it[f]);
@@ -510,7 +622,41 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
       ctx->it[f] = tmp;
     }
   }
-  ctx->t = t + tau;
+  ctx->t += ctx->dt;
+}
+
+// One time step of a group of contexts that together hold both patches: one
+// context (both patches, or one NCCL rank), or a loopback pair.  Every stage
+// runs on every context before the next (the exchange needs all donors done).
+yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* rho_out) {
+  yy_ctx* ctx = cs[0];
+  for (yy_ctx* c : cs) TRY(step_begin(c));
+  const int kmax = ctx->fixed_iters > 0 ? ctx->fixed_iters : ctx->max_iters;
+  int k = 0;
+  double rho = INFINITY;
+  while (k < kmax) {
+    ++k;
+    TRY(exchange_fringe(cs));                              // O5
+    for (yy_ctx* c : cs) TRY(iter_solve(c));               // O6-O9, local norms
+    TRY(reduce_group(cs));                                 // O10
+    for (yy_ctx* c : cs) {
+      yy_ctx* ctx = c;
+      CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    for (yy_ctx* c : cs) {
+      yy_ctx* ctx = c;
+      CK(cudaStreamSynchronize(c->st));
+      if (c->prof_on) prof_collect(c);
+    }
+    rho = ctx->red_host[0];
+    if (ctx->red_host[1] != 0.0) {
+      for (yy_ctx* c : cs) fail(c, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
+      return YY_ESOLVER;
+    }
+    if (ctx->fixed_iters <= 0 && rho < tol) break;
+  }
+  for (yy_ctx* c : cs) step_end(c);
   *iters = k;
   *rho_out = rho;
   return YY_OK;
@@ -521,9 +667,9 @@ yy_status one_step(yy_ctx* ctx, double tol, int* iters, double* rho_out) {
 // =====================================================================================
 // C ABI
 // =====================================================================================
-extern "C" {
-
-yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, yy_ctx** out) {
+namespace {
+yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, int npatch,
+                     int patch0, yy_ctx** out) {
   if (!out) return YY_EINVAL;
   *out = nullptr;
   if (!gr || gr->nr < 2 || gr->ntheta < 8 || gr->nphi < 8) return YY_EINVAL;
@@ -538,6 +684,8 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   HostGeo h = host_geo(gr, R1, R2);
   Geo& g = ctx->g;
   g.nr = h.nr; g.nt = h.nt; g.np = h.np;
+  g.npatch = npatch;
+  ctx->patch0 = patch0;
   g.dr = h.dr; g.dth = h.dth; g.dph = h.dph; g.R1 = R1;
   g.tau = dt; g.nu = Pr; g.kap = 1.0;
   g.cchi = 1.0 / (2.0 * ctx->chi); g.inv_chi = 1.0 / ctx->chi; g.PrRa = Pr * Ra;
@@ -611,7 +759,7 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   long long maxk = 0;
   for (int K = 0; K < 4; ++K) maxk = std::max(maxk, psize(g, K));
   for (int f = 0; f < NF; ++f) {
-    const size_t sz = 2 * psize(g, FKIND[f]);
+    const size_t sz = (size_t)npatch * psize(g, FKIND[f]);
     if ((s = dalloc(ctx, &ctx->n[f], sz)) != YY_OK || (s = dalloc(ctx, &ctx->it[f], sz)) != YY_OK) { yy_destroy(ctx); return s; }
     if (f != FP1 && f != FP2) {
       if ((s = dalloc(ctx, &ctx->m[f], sz)) != YY_OK || (s = dalloc(ctx, &ctx->G[f], sz)) != YY_OK) { yy_destroy(ctx); return s; }
@@ -622,9 +770,9 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
     if (ctx->G[f]) cudaMemset(ctx->G[f], 0, sz * sizeof(double));
   }
   for (int c = 0; c < 3; ++c)
-    if ((s = dalloc(ctx, &ctx->astar[c], 2 * psize(g, KR + c))) != YY_OK) { yy_destroy(ctx); return s; }
-  if ((s = dalloc(ctx, &ctx->R, 2 * maxk)) != YY_OK || (s = dalloc(ctx, &ctx->C, 2 * maxk)) != YY_OK) { yy_destroy(ctx); return s; }
-  cudaMemset(ctx->R, 0, 2 * maxk * sizeof(double));
+    if ((s = dalloc(ctx, &ctx->astar[c], npatch * psize(g, KR + c))) != YY_OK) { yy_destroy(ctx); return s; }
+  if ((s = dalloc(ctx, &ctx->R, npatch * maxk)) != YY_OK) { yy_destroy(ctx); return s; }
+  cudaMemset(ctx->R, 0, npatch * maxk * sizeof(double));
   // norm partials: max blocks per (slot, patch)
   long long mb = 0;
   for (int K = 0; K < 4; ++K) {
@@ -639,9 +787,79 @@ yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double R
   if (cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) { yy_destroy(ctx); return YY_ENOMEM; }
   for (int L = 0; L < 3; ++L)
     for (int f = 0; f < NW; ++f)
-      if ((s = dalloc(ctx, &ctx->wl[L][f], 4 * wsize(g, WKIND[f]))) != YY_OK) { yy_destroy(ctx); return s; }
+      if ((s = dalloc(ctx, &ctx->wl[L][f], 2 * npatch * wsize(g, WKIND[f]))) != YY_OK) { yy_destroy(ctx); return s; }
+  if (npatch == 1) {   // fringe transfer buffers of a one-patch context
+    InterpArgs ia{};
+    ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
+    ctx->fr_n = fringe_count(g, ia);
+    if ((s = dalloc(ctx, &ctx->fr_send, ctx->fr_n)) != YY_OK || (s = dalloc(ctx, &ctx->fr_recv, ctx->fr_n)) != YY_OK ||
+        (s = dalloc(ctx, &ctx->peer_red, 2 + 2 * NSLOT)) != YY_OK) { yy_destroy(ctx); return s; }
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
   *out = ctx;
+  return YY_OK;
+}
+}  // namespace
+
+extern "C" {
+
+yy_status yy_create(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, yy_ctx** out) {
+  return create_ctx(gr, R1, R2, Pr, Ra, dt, 2, 0, out);
+}
+
+yy_status yy_nccl_unique_id(void* out128) {
+  if (!out128) return YY_EINVAL;
+  NcclApi& N = nccl_api();
+  if (!N.ok) return YY_ENCCL;
+  ncclUniqueId id;
+  if (N.GetUniqueId(&id) != ncclSuccess) return YY_ENCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return YY_OK;
+}
+
+yy_status yy_create_dist(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, int32_t world,
+                         int32_t rank, const void* nccl_id, int32_t device, yy_ctx** out) {
+  if (!out) return YY_EINVAL;
+  *out = nullptr;
+  if (world == 1 && rank == 0) {
+    if (cudaSetDevice(device) != cudaSuccess) return YY_ECUDA;
+    return yy_create(gr, R1, R2, Pr, Ra, dt, out);
+  }
+  // one rank per patch (Yin = rank 0, Yang = rank 1); radial slabs (world 4, 8) are not built
+  if (world != 2 || rank < 0 || rank > 1 || !nccl_id) return YY_EINVAL;
+  NcclApi& N = nccl_api();
+  if (!N.ok) return YY_ENCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return YY_ECUDA;
+  yy_ctx* ctx = nullptr;
+  yy_status s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, rank, &ctx);
+  if (s != YY_OK) return s;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  if (N.CommInitRank(&comm, world, id, rank) != ncclSuccess) {
+    yy_destroy(ctx);
+    return YY_ENCCL;
+  }
+  ctx->nccl = comm;
+  ctx->mode = 2;
+  ctx->world = world;
+  ctx->rank = rank;
+  *out = ctx;
+  return YY_OK;
+}
+
+yy_status yy_create_pair(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, yy_ctx** out2) {
+  if (!out2) return YY_EINVAL;
+  out2[0] = out2[1] = nullptr;
+  yy_status s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, 0, &out2[0]);
+  if (s != YY_OK) return s;
+  s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, 1, &out2[1]);
+  if (s != YY_OK) { yy_destroy(out2[0]); out2[0] = nullptr; return s; }
+  out2[0]->mode = out2[1]->mode = 1;
+  out2[0]->peer = out2[1];
+  out2[1]->peer = out2[0];
+  out2[1]->st = out2[0]->st;
   return YY_OK;
 }
 
@@ -653,7 +871,7 @@ yy_status yy_set_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t syste
   auto put = [&](int fidx, const double* src) -> yy_status {
     if (!src) return YY_OK;
     const long long sz = fsize(ctx, fidx);
-    CK(cudaMemcpy(L[fidx] + patch * sz, src, sz * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(L[fidx] + (patch - ctx->patch0) * sz, src, sz * sizeof(double), cudaMemcpyHostToDevice));
     return YY_OK;
   };
   for (int s = sys_lo; s <= sys_hi; ++s) {
@@ -674,7 +892,7 @@ yy_status yy_get_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t syste
   auto get = [&](int fidx, double* dst) -> yy_status {
     if (!dst) return YY_OK;
     const long long sz = fsize(ctx, fidx);
-    CK(cudaMemcpy(dst, L[fidx] + patch * sz, sz * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(dst, L[fidx] + (patch - ctx->patch0) * sz, sz * sizeof(double), cudaMemcpyDeviceToHost));
     return YY_OK;
   };
   const int o = (system == 2) ? 3 : 0;
@@ -692,6 +910,9 @@ static yy_status set_terms(yy_ctx* ctx, int32_t patch, int32_t nterms, const int
   if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
   if (patch < 0 || patch > 1 || nterms < 0 || nterms > MAXSRC || (nterms > 0 && (!timefn || !terms)))
     return fail(ctx, YY_EINVAL, "bad wall/source terms");
+  if (patch < ctx->patch0 || patch >= ctx->patch0 + ctx->g.npatch)
+    return fail(ctx, YY_EINVAL, "this context does not hold that patch");
+  patch -= ctx->patch0;   // local index
   const Geo& g = ctx->g;
   for (int m = 0; m < nterms; ++m)
     if (timefn[m] < YY_TF_ONE || timefn[m] > YY_TF_COS2) return fail(ctx, YY_EINVAL, "bad time function");
@@ -750,6 +971,7 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
 yy_status yy_set_stream(yy_ctx* ctx, void* stream) {
   if (!ctx) return YY_EINVAL;
   ctx->st = static_cast<cudaStream_t>(stream);
+  if (ctx->mode == 1 && ctx->peer) ctx->peer->st = ctx->st;   // a loopback pair shares one stream
   return YY_OK;
 }
 
@@ -757,13 +979,26 @@ yy_status yy_step(yy_ctx* ctx, int32_t nsteps, double tol) {
   if (!ctx) return YY_EINVAL;
   if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
   if (nsteps < 0 || !(tol > 0)) return fail(ctx, YY_EINVAL, "nsteps >= 0 and tol > 0 required");
+  // the group that holds both patches: this context, or a loopback pair (Yin first)
+  std::vector<yy_ctx*> cs{ctx};
+  if (ctx->mode == 1) {
+    if (!ctx->peer) return fail(ctx, YY_ESTATE, "loopback partner destroyed");
+    if (ctx->peer->dead) return fail(ctx, YY_ESTATE, "loopback partner unusable");
+    cs = ctx->patch0 == 0 ? std::vector<yy_ctx*>{ctx, ctx->peer} : std::vector<yy_ctx*>{ctx->peer, ctx};
+  }
   yy_status res = YY_OK;
   for (int s = 0; s < nsteps; ++s) {
     int it = 0;
     double rho = 0;
-    TRY(one_step(ctx, tol, &it, &rho));
-    ctx->st_iters.push_back(it);
-    ctx->st_rho.push_back(rho);
+    yy_status r = step_group(cs, tol, &it, &rho);
+    if (r != YY_OK) {
+      if (ctx->err.empty()) for (yy_ctx* c : cs) if (!c->err.empty()) ctx->err = c->err;
+      return r;
+    }
+    for (yy_ctx* c : cs) {
+      c->st_iters.push_back(it);
+      c->st_rho.push_back(rho);
+    }
     if (ctx->fixed_iters <= 0 && !(rho < tol)) res = YY_ENOCONV;
   }
   return res;
@@ -803,6 +1038,8 @@ const char* yy_last_error(const yy_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 
 void yy_destroy(yy_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->mode == 1 && ctx->peer) ctx->peer->peer = nullptr;
+  if (ctx->mode == 2 && ctx->nccl) nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->nccl));
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->red_host) cudaFreeHost(ctx->red_host);
   delete ctx;
@@ -810,7 +1047,8 @@ void yy_destroy(yy_ctx* ctx) {
 
 // ---- test / kernel-only entry points (include/yy_test.h) ---------------------------
 yy_status yy_debug_get(yy_ctx* ctx, const char* name, int32_t patch, double* host) {
-  if (!ctx || !name || !host || patch < 0 || patch > 1) return YY_EINVAL;
+  if (!ctx || !name || !host || patch < ctx->patch0 || patch >= ctx->patch0 + ctx->g.npatch) return YY_EINVAL;
+  patch -= ctx->patch0;
   const Geo& g = ctx->g;
   const double* src = nullptr;
   long long sz = 0;

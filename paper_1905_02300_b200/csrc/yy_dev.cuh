@@ -22,6 +22,7 @@ __host__ __device__ constexpr int kind_of(int q) { return q; }   // Quant -> Kin
 // Geometry + physics, passed by value to every kernel.
 struct Geo {
   int nr, nt, np;                 // cells per patch
+  int npatch;                     // patches held by this context: 2 (both), 1 (one rank per patch)
   double dr, dth, dph, R1;
   double tau, nu, kap, cchi, inv_chi, PrRa;
   double hatph;                   // 1/(R1^2 sin^2(theta_1) dph^2), theta_1 = pi/4 - delta (RD31)

@@ -67,6 +67,8 @@ struct PresArgs {
 struct ReduceArgs {
   int nblk[NSLOT];
   int maxb;
+  int npatch;                // local patches
+  int patch0;                // global id of local patch 0 (sums land at out[2 + 2 slot + patch])
 };
 
 struct CCTab {               // fringe of kinds C / R on the (theta_c, phi_c) lattice
@@ -114,7 +116,18 @@ inline int launch_sweep(const Geo& g, int q, int ax, int s, bool first, bool fin
 }
 #endif
 int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st);
-void launch_reduce(const double* part, const ReduceArgs& a, double* out, cudaStream_t st);
+// per-(slot, local patch) sums of the norm partials -> out[2 + 2 slot + patch]
+void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, cudaStream_t st);
+// rho = max over the 2 NSLOT sums -> out[0], NaN flag -> out[1]
+void launch_reduce_final(double* out, cudaStream_t st);
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st);
+// one patch per context: the donor evaluates the partner's fringe values from its
+// own patch into buf (pack), the target writes a received buf into its fringe
+// (unpack).  Layout: [cc: 5 x (nr+1) x n_cc][th: 2 x nr x n_th][ph: 2 x nr x n_ph].
+long long fringe_count(const Geo& g, const InterpArgs& a);
+void launch_fringe_pack(const Geo& g, const InterpArgs& a, double* buf, cudaStream_t st);
+void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, cudaStream_t st);
+// out[2 + 2 slot + peer_patch] <- peer[2 + 2 slot + peer_patch] (the partner's sums)
+void launch_merge_sums(double* out, const double* peer, int peer_patch, cudaStream_t st);
 
 }  // namespace yy

@@ -198,13 +198,17 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_reduce_slots(const double* __restrict__ part, ReduceArgs a,
                                                       double* __restrict__ out) {
-  const int slot = blockIdx.x / 2, patch = blockIdx.x % 2;   // one block per (slot, patch)
-  const double* p = part + ((long long)slot * 2 + patch) * a.maxb;
+  const int slot = blockIdx.x / a.npatch, lp = blockIdx.x % a.npatch;   // one block per (slot, local patch)
+  const double* p = part + ((long long)slot * 2 + lp) * a.maxb;
   const int nb = a.nblk[slot];
   double v = 0.0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) v += p[b];
   const double t = block_sum<256>(v);
-  if (threadIdx.x == 0) out[2 + blockIdx.x] = t;
+  if (threadIdx.x == 0) out[2 + 2 * slot + lp + a.patch0] = t;
+}
+
+__global__ void k_merge_sums(double* __restrict__ out, const double* __restrict__ peer, int pp) {
+  if (threadIdx.x < NSLOT) out[2 + 2 * threadIdx.x + pp] = peer[2 + 2 * threadIdx.x + pp];
 }
 
 __global__ void k_reduce_final(double* __restrict__ out) {
@@ -280,6 +284,52 @@ __global__ void k_interp_vec(Geo g, InterpArgs a) {
   tgt[((long long)i * NTk(g, KTGT) + t.tj[e]) * NPk(g, KTGT) + t.tk[e]] = v;
 }
 
+// ---- one patch per context: donor-side evaluation + transfer + target write ----
+// The fringe tables are the same in both directions (the patches are congruent
+// and the chart map is an involution), so the donor evaluates the
+// partner's fringe with the partner's own entries, from its local patch.
+// grid: x -> entry, y -> i, z -> quantity
+__global__ void k_pack_cc(Geo g, InterpArgs a, double* __restrict__ buf) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, q = blockIdx.z;
+  if (e >= a.tab_cc.n) return;
+  const int K = (q < 3) ? KC : KR;
+  if (K == KC && i >= g.nr) return;
+  if (K == KR && (i < 1 || i > g.nr - 1)) return;
+  const int jb = a.tab_cc.jb[e], kb = a.tab_cc.kb[e];
+  buf[((long long)q * (g.nr + 1) + i) * a.tab_cc.n + e] = interp16(g, K, a.cc[q], i, jb, kb, a.tab_cc.w + 8LL * e);
+}
+__global__ void k_unpack_cc(Geo g, InterpArgs a, const double* __restrict__ buf) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, q = blockIdx.z;
+  if (e >= a.tab_cc.n) return;
+  const int K = (q < 3) ? KC : KR;
+  if (K == KC && i >= g.nr) return;
+  if (K == KR && (i < 1 || i > g.nr - 1)) return;
+  a.cc[q][((long long)i * NTk(g, K) + a.tab_cc.tj[e]) * NPk(g, K) + a.tab_cc.tk[e]] =
+      buf[((long long)q * (g.nr + 1) + i) * a.tab_cc.n + e];
+}
+// grid: x -> entry, y -> i, z -> system
+template <int KTGT>
+__global__ void k_pack_vec(Geo g, InterpArgs a, double* __restrict__ buf) {
+  const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, s = blockIdx.z;
+  if (e >= t.n) return;
+  const double vt = interp16(g, KT, a.ut[s], i, t.jb_t[e], t.kb_t[e], t.w_t + 8LL * e);
+  const double vp = interp16(g, KP, a.up[s], i, t.jb_p[e], t.kb_p[e], t.w_p + 8LL * e);
+  buf[((long long)s * g.nr + i) * t.n + e] = t.m0[e] * vt + t.m1[e] * vp;
+}
+template <int KTGT>
+__global__ void k_unpack_vec(Geo g, InterpArgs a, const double* __restrict__ buf) {
+  const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, s = blockIdx.z;
+  if (e >= t.n) return;
+  double* tgt = (KTGT == KT) ? a.ut[s] : a.up[s];
+  tgt[((long long)i * NTk(g, KTGT) + t.tj[e]) * NPk(g, KTGT) + t.tk[e]] = buf[((long long)s * g.nr + i) * t.n + e];
+}
+
 // ---------------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------------
@@ -296,10 +346,10 @@ void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStre
 
 void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st) {
   switch (q) {
-    case QT: k_static<QT><<<pgrid(g, KC, 2), 128, 0, st>>>(g, a); break;
-    case QUR: k_static<QUR><<<pgrid(g, KR, 2), 128, 0, st>>>(g, a); break;
-    case QUT: k_static<QUT><<<pgrid(g, KT, 2), 128, 0, st>>>(g, a); break;
-    case QUP: k_static<QUP><<<pgrid(g, KP, 2), 128, 0, st>>>(g, a); break;
+    case QT: k_static<QT><<<pgrid(g, KC, g.npatch), 128, 0, st>>>(g, a); break;
+    case QUR: k_static<QUR><<<pgrid(g, KR, g.npatch), 128, 0, st>>>(g, a); break;
+    case QUT: k_static<QUT><<<pgrid(g, KT, g.npatch), 128, 0, st>>>(g, a); break;
+    case QUP: k_static<QUP><<<pgrid(g, KP, g.npatch), 128, 0, st>>>(g, a); break;
   }
 }
 
@@ -307,7 +357,7 @@ template <int Q, int S, int IB>
 void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   const int nch = (i_hi<K>(g) - i_lo<K>() + IB) / IB;
-  const dim3 grid((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, 2 * nch);
+  const dim3 grid((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, g.npatch * nch);
   k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
 }
 // r-nodes per thread of the residual, per quantity (measured on B200, C3);
@@ -334,21 +384,46 @@ void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t s
 
 int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st) {
   const int nz = (g.nr + 3) / 4;
-  dim3 grid((g.np + 127) / 128, g.nt, 2 * nz);
+  dim3 grid((g.np + 127) / 128, g.nt, g.npatch * nz);
   if (s == 1) k_pres<1><<<grid, 128, 0, st>>>(g, a);
   else k_pres<2><<<grid, 128, 0, st>>>(g, a);
   return (int)(grid.x * grid.y * nz);
 }
 
-void launch_reduce(const double* part, const ReduceArgs& a, double* out, cudaStream_t st) {
-  k_reduce_slots<<<2 * NSLOT, 256, 0, st>>>(part, a, out);
-  k_reduce_final<<<1, 32, 0, st>>>(out);
+void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, cudaStream_t st) {
+  k_reduce_slots<<<a.npatch * NSLOT, 256, 0, st>>>(part, a, out);
 }
+
+void launch_reduce_final(double* out, cudaStream_t st) { k_reduce_final<<<1, 32, 0, st>>>(out); }
 
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st) {
   if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 10), 128, 0, st>>>(g, a);
   if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, g.nr, 4), 128, 0, st>>>(g, a);
   if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 4), 128, 0, st>>>(g, a);
+}
+
+long long fringe_count(const Geo& g, const InterpArgs& a) {
+  return 5LL * (g.nr + 1) * a.tab_cc.n + 2LL * g.nr * a.tab_th.n + 2LL * g.nr * a.tab_ph.n;
+}
+
+void launch_fringe_pack(const Geo& g, const InterpArgs& a, double* buf, cudaStream_t st) {
+  double* bth = buf + 5LL * (g.nr + 1) * a.tab_cc.n;
+  double* bph = bth + 2LL * g.nr * a.tab_th.n;
+  if (a.tab_cc.n) k_pack_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 5), 128, 0, st>>>(g, a, buf);
+  if (a.tab_th.n) k_pack_vec<KT><<<dim3((a.tab_th.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bth);
+  if (a.tab_ph.n) k_pack_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bph);
+}
+
+void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, cudaStream_t st) {
+  const double* bth = buf + 5LL * (g.nr + 1) * a.tab_cc.n;
+  const double* bph = bth + 2LL * g.nr * a.tab_th.n;
+  if (a.tab_cc.n) k_unpack_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 5), 128, 0, st>>>(g, a, buf);
+  if (a.tab_th.n) k_unpack_vec<KT><<<dim3((a.tab_th.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bth);
+  if (a.tab_ph.n) k_unpack_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bph);
+}
+
+void launch_merge_sums(double* out, const double* peer, int peer_patch, cudaStream_t st) {
+  k_merge_sums<<<1, 32, 0, st>>>(out, peer, peer_patch);
 }
 
 }  // namespace yy

@@ -76,7 +76,11 @@ def load_library():
     L.yy_launch_count.argtypes = [ctx]
     L.yy_launch_count.restype = ctypes.c_int64
     L.yy_profile_report.argtypes = [ctx, ctypes.c_char_p, c_int32]
-    for name in ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
+    L.yy_create_pair.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double, c_void_p]
+    L.yy_create_dist.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double,
+                                 c_int32, c_int32, c_void_p, c_int32, POINTER(ctx)]
+    L.yy_nccl_unique_id.argtypes = [c_void_p]
+    for name in ("yy_create_pair", "yy_create_dist", "yy_nccl_unique_id", "yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
                  "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve",
                  "yy_profile_report"):
         getattr(L, name).restype = c_int32
@@ -92,15 +96,57 @@ class Shell:
     """One Yin-Yang shell context (include/yy.h `yy_ctx`)."""
 
     def __init__(self, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3,
-                 chi=None, max_iters=None, fixed_iters=None, stream=None):
+                 chi=None, max_iters=None, fixed_iters=None, stream=None, _handle=None, _patches=(0, 1)):
         self.L = load_library()
         self.nr, self.nt, self.np_ = nr, ntheta, nphi
+        self.patches = tuple(_patches)        # patches this context holds
+        if _handle is None:
+            g = yy_grid(nr, ntheta, nphi)
+            h = c_void_p()
+            st = self.L.yy_create(ctypes.byref(g), R1, R2, Pr, Ra, dt, ctypes.byref(h))
+            if st != YY_OK:
+                raise YYError(f"yy_create failed with status {st}")
+            _handle = h
+        self.h = _handle
+        if chi is not None:
+            self.set_param(YY_CHI, chi)
+        if max_iters is not None:
+            self.set_param(YY_MAX_ITERS, max_iters)
+        if fixed_iters is not None:
+            self.set_param(YY_FIXED_ITERS, fixed_iters)
+        if stream is not None:
+            self.set_stream(stream)
+
+    @classmethod
+    def pair(cls, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3, **kw):
+        """yy_create_pair (include/yy_test.h): (Yin, Yang) one-patch contexts on this
+        device exchanging through device copies — the yy_create_dist data path."""
+        L = load_library()
+        g = yy_grid(nr, ntheta, nphi)
+        hs = (c_void_p * 2)()
+        st = L.yy_create_pair(ctypes.byref(g), R1, R2, Pr, Ra, dt, hs)
+        if st != YY_OK:
+            raise YYError(f"yy_create_pair failed with status {st}")
+        out = [cls(nr, ntheta, nphi, _handle=c_void_p(hs[p]), _patches=(p,)) for p in range(2)]
+        for sh in out:
+            sh._configure(**kw)
+        return out
+
+    @classmethod
+    def dist(cls, nr, ntheta, nphi, R1, R2, Pr, Ra, dt, world, rank, nccl_id, device, **kw):
+        """yy_create_dist: rank `rank` of `world` (2: one patch per rank) over NCCL."""
+        L = load_library()
         g = yy_grid(nr, ntheta, nphi)
         h = c_void_p()
-        st = self.L.yy_create(ctypes.byref(g), R1, R2, Pr, Ra, dt, ctypes.byref(h))
+        idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        st = L.yy_create_dist(ctypes.byref(g), R1, R2, Pr, Ra, dt, world, rank, idb, device, ctypes.byref(h))
         if st != YY_OK:
-            raise YYError(f"yy_create failed with status {st}")
-        self.h = h
+            raise YYError(f"yy_create_dist failed with status {st}")
+        sh = cls(nr, ntheta, nphi, _handle=h, _patches=(rank,) if world == 2 else (0, 1))
+        sh._configure(**kw)
+        return sh
+
+    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None):
         if chi is not None:
             self.set_param(YY_CHI, chi)
         if max_iters is not None:
@@ -232,6 +278,8 @@ class Shell:
     def load_workload(self, wl):
         """Upload a workloads.make_workload() dict (levels, walls, sources)."""
         for patch, pd in enumerate(wl["patches"]):
+            if patch not in self.patches:
+                continue
             n = pd["n"]
             self.set_fields(patch, 0, 1, ur=n["ur"], ut=n["ut"], up=n["up"], T=n["T"], p=n["p1"])
             self.set_fields(patch, 0, 2, ur=n["ur"], ut=n["ut"], up=n["up"], p=n["p2"])
@@ -239,3 +287,13 @@ class Shell:
             self.set_fields(patch, 1, 0, **{k: m[k] for k in ("ur", "ut", "up", "T")})
             self.set_wall(patch, pd["walls"])
             self.set_source(patch, pd["sources"])
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id for yy_create_dist (call on rank 0, broadcast it)."""
+    L = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = L.yy_nccl_unique_id(buf)
+    if st != YY_OK:
+        raise YYError(f"yy_nccl_unique_id failed with status {st} (NCCL not loadable?)")
+    return buf.raw

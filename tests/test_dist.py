@@ -1,0 +1,118 @@
+"""Multi-GPU layout, one patch per rank.
+
+CPU (gloo, world size 2): the host plumbing — rank -> patch plan and the NCCL
+unique-id handshake through torch.distributed — is the same on every rank.
+
+GPU (one device): yy_create_pair runs the distributed data path (donor-side
+fringe evaluation, transfer, target write, fixed-order norm merge) with two
+one-patch contexts exchanging by device copies.  It must reproduce the
+single-context step bit for bit (same kernels, same operands) and therefore the
+oracle within the parity bar, with identical Schwarz iteration counts."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as td
+import torch.multiprocessing as mp
+
+import workloads as W
+from oracle.scheme import Oracle
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1905_02300_b200 import dist
+        uid = dist.share_unique_id(rank)
+        q.put((rank, dist.plan(world, rank), uid))
+    finally:
+        td.destroy_process_group()
+
+
+def test_plan_and_unique_id_handshake_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict()
+    for _ in range(2):
+        r, plan, uid = q.get(timeout=120)
+        got[r] = (plan, uid)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert got[0][0] == {"patches": (0,), "partner": 1}
+    assert got[1][0] == {"patches": (1,), "partner": 0}
+    assert len(got[0][1]) == 128 and got[0][1] == got[1][1] and any(got[0][1])
+
+
+def test_plan_rejects_unbuilt_worlds():
+    from paper_1905_02300_b200 import dist
+    assert dist.plan(1, 0) == {"patches": (0, 1), "partner": None}
+    for world in (3, 4, 8):
+        with pytest.raises(ValueError):
+            dist.plan(world, 0)
+
+
+def _fields_all(shells, p, lev, s):
+    for sh in shells:
+        if p in sh.patches:
+            return sh.get_fields(p, lev, s)
+    raise AssertionError(p)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["c1", "convection", "random"])
+def test_pair_reproduces_single_context_and_oracle(case):
+    from paper_1905_02300_b200 import Shell
+    if case == "c1":
+        cfg, wl, steps = W.config("C1"), None, 2
+    elif case == "convection":
+        cfg, wl, steps = W.small("C3", 10, 18, 50), None, 2
+    else:
+        cfg = W.small("C1", 7, 13, 37, Ra=30.0, dt=2e-3)
+        wl, steps = W.random_state(cfg, seed=11, amp=5.0), 2
+    wl = wl if wl is not None else W.make_workload(cfg)
+    args = (cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    one = Shell(*args)
+    one.load_workload(wl)
+    pair = Shell.pair(*args)
+    for sh in pair:
+        sh.load_workload(wl)
+    o = Oracle(*args)
+    o.load_workload(wl)
+    for _ in range(steps):
+        one.step(1, cfg.tol)
+        pair[0].step(1, cfg.tol)           # advances both members
+        o.step(1, cfg.tol)
+        assert pair[0].stats()[-1] == one.stats()[-1] == pair[1].stats()[-1]
+        assert one.stats()[-1][0] == o.stats[-1][0]
+        for p in range(2):
+            for s in (1, 2):
+                a = one.get_fields(p, 0, s)
+                b = _fields_all(pair, p, 0, s)
+                c = o.get_fields(p, 0, s)
+                vmax = max(np.max(np.abs(c[q])) for q in ("ur", "ut", "up"))
+                for k in a:
+                    assert np.array_equal(a[k], b[k]), (p, s, k)
+                    den = vmax if k in ("ur", "ut", "up") else max(np.max(np.abs(c[k])), 1e-300)
+                    assert np.max(np.abs(b[k] - c[k])) / den <= 1e-11, (p, s, k)
+
+
+@pytest.mark.gpu
+def test_pair_members_only_accept_their_patch():
+    from paper_1905_02300_b200 import Shell, YYError
+    cfg = W.small("C1", 4, 12, 28)
+    yin, yang = Shell.pair(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    with pytest.raises(YYError):
+        yin.set_fields(1, 0, 0, T=np.zeros((4, 12, 28)))
+    with pytest.raises(YYError):
+        yang.get_fields(0, 0, 2)
+    yang.close()
+    with pytest.raises(YYError):      # partner gone
+        yin.step(1, 1e-10)
