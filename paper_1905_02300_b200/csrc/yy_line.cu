@@ -32,6 +32,10 @@
 #include "yy_internal.h"
 #include "yy_stencil.cuh"
 
+#ifndef YY_LINE_MINB
+#define YY_LINE_MINB 0   // >0: force this __launch_bounds__ min blocks per SM (tuning)
+#endif
+
 namespace yy {
 
 namespace {
@@ -191,8 +195,15 @@ __host__ __device__ constexpr int line_pitch() {
 // ---------------------------------------------------------------------------------
 enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2 };
 
+// resident 128-thread blocks per SM the register allocation must allow (the
+// chunk arrays are 6 M registers): measured on B200 (C3), 96 registers for
+// chunks of <= 12 rows beat the unconstrained ~130 (occupancy over ILP)
+constexpr int line_minb(int M) {
+  return YY_LINE_MINB > 0 ? YY_LINE_MINB : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 3 : 2);
+}
+
 template <int Q, int AX, int MODE, int S, int P, int M>
-__global__ void __launch_bounds__(128) k_line(Geo g, SweepArgs a, ResidArgs ra) {
+__global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, ResidArgs ra) {
   constexpr bool FINAL = (MODE == MODE_FINAL);
   constexpr int K = kind_of(Q);
   constexpr int NL = 128 / P;

@@ -40,7 +40,8 @@ class yy_fields(ctypes.Structure):
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libyy.so")
+    # YY_LIB: an alternative build of the same library (tuning experiments only)
+    return os.environ.get("YY_LIB") or os.path.join(_HERE, "libyy.so")
 
 
 _lib = None
