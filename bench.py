@@ -140,6 +140,18 @@ def m1_bytes(name, cfg, nsrc):
     return 0
 
 
+def traffic_of(name, workload):
+    """DRAM bytes per launch of a kernel class from the committed ncu capture
+    (profiles/traffic.json), or None."""
+    if workload != "C3":
+        return None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            return json.load(f)["bytes_per_launch"].get(name)
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def step_model_bytes(cfg, K, forced):
     """M1 bytes of one full step with K Schwarz iterations."""
     per_cell = (352 if forced else 256) + 1320 * K
@@ -334,7 +346,9 @@ def run_yy(args):
                                      "frac_of_8TBs": t_roof_8 / (ms / 1e3),
                                      "frac_of_measured_hbm": t_roof_m / (ms / 1e3)}},
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic_of(dname, args.workload),
+                     "traffic_source": "profiles/traffic.json (ncu --set full capture of this kernel class, C3)",
                      "peak_source": peak_kind, "bytes_per_launch": dbytes, "avg_launch_ms": davg_s * 1e3,
                      "launches": dcount, "share_of_step": share},
         "kernel_classes": {k: {"launches": n, "ms": t, "GBps": (m1_bytes(k, cfg, nsrc) * n / (t / 1e3) / 1e9)

@@ -16,3 +16,7 @@ if [ -n "${NCU_K:-}" ]; then
 B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$NCU_K" -s ${NCU_S:-3000} -c ${NCU_C:-14} -o gpurun_out/prof_try $B > gpurun_out/ncu_try.log 2>&1; echo "ncu rc $?" >> gpurun_out/rc.txt
 fi
+if [ -n "${NCU_DEM:-}" ]; then   # capture kernels by demangled-name regex (template args included)
+B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$NCU_DEM" -s ${NCU_S:-0} -c ${NCU_C:-3} -o gpurun_out/prof_dem $B > gpurun_out/ncu_dem.log 2>&1; echo "ncu_dem rc $?" >> gpurun_out/rc.txt
+fi
