@@ -686,6 +686,9 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   g.nr = h.nr; g.nt = h.nt; g.np = h.np;
   g.npatch = npatch;
   ctx->patch0 = patch0;
+  g.ilo_c = 0; g.ihi_c = h.nr - 1; g.ilo_f = 1; g.ihi_f = h.nr - 1;
+  g.wall_lo = g.wall_hi = 1;
+  g.ifr_c0 = 0; g.ifr_c1 = h.nr - 1; g.ifr_f0 = 1; g.ifr_f1 = h.nr - 1;
   g.dr = h.dr; g.dth = h.dth; g.dph = h.dph; g.R1 = R1;
   g.tau = dt; g.nu = Pr; g.kap = 1.0;
   g.cchi = 1.0 / (2.0 * ctx->chi); g.inv_chi = 1.0 / ctx->chi; g.PrRa = Pr * Ra;

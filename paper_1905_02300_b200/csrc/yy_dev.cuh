@@ -23,6 +23,12 @@ __host__ __device__ constexpr int kind_of(int q) { return q; }   // Quant -> Kin
 struct Geo {
   int nr, nt, np;                 // cells per patch
   int npatch;                     // patches held by this context: 2 (both), 1 (one rank per patch)
+  // local r-rows of this context (a radial slab keeps one halo row on each side;
+  // the whole shell: ilo_c = 0, ihi_c = nr-1, ilo_f = 1, ihi_f = nr-1, walls both)
+  int ilo_c, ihi_c;               // solved rows of r-centred kinds (C, TH, PH)
+  int ilo_f, ihi_f;               // solved r-faces (u_r)
+  int wall_lo, wall_hi;           // this context's rows touch r = R1 / r = R2
+  int ifr_c0, ifr_c1, ifr_f0, ifr_f1;   // rows whose fringe nodes are interpolated
   double dr, dth, dph, R1;
   double tau, nu, kap, cchi, inv_chi, PrRa;
   double hatph;                   // 1/(R1^2 sin^2(theta_1) dph^2), theta_1 = pi/4 - delta (RD31)
@@ -209,7 +215,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
 
 // Solved-node ranges of a kind (reading RD3): fringe = outermost theta/phi
 // layer; u_r wall faces excluded.
-template <int K> __host__ __device__ __forceinline__ int i_lo() { return K == KR ? 1 : 0; }
-template <int K> __host__ __device__ __forceinline__ int i_hi(const Geo& g) { return K == KR ? g.nr - 1 : g.nr - 1; }
+template <int K> __host__ __device__ __forceinline__ int i_lo(const Geo& g) { return K == KR ? g.ilo_f : g.ilo_c; }
+template <int K> __host__ __device__ __forceinline__ int i_hi(const Geo& g) { return K == KR ? g.ihi_f : g.ihi_c; }
 
 }  // namespace yy

@@ -138,9 +138,9 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
   constexpr int K = kind_of(Q);
   const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   const int j = blockIdx.y + 1;
-  const int nch = (i_hi<K>(g) - i_lo<K>() + IB) / IB;
+  const int nch = (i_hi<K>(g) - i_lo<K>(g) + IB) / IB;
   const int patch = blockIdx.z / nch;
-  const int i0 = i_lo<K>() + (blockIdx.z % nch) * IB;
+  const int i0 = i_lo<K>(g) + (blockIdx.z % nch) * IB;
   if (k > NPk(g, K) - 2) return;
   double* __restrict__ R = a.R + patch * psize(g, K);
 #pragma unroll
@@ -157,8 +157,8 @@ template <int S>
 __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
-  const int nz = (g.nr + 3) / 4;
-  const int patch = blockIdx.z / nz, i0 = 4 * (blockIdx.z % nz);
+  const int nz = (g.ihi_c - g.ilo_c + 4) / 4;
+  const int patch = blockIdx.z / nz, i0 = g.ilo_c + 4 * (blockIdx.z % nz);
   double w = 0.0;
   if (k >= 1 && k <= g.np - 2 && j >= 1 && j <= g.nt - 2) {
     const long long pc = patch * psize(g, KC);
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
     const double *uti = a.utit + ot, *utn = a.utn + ot;
     const double *upi = a.upit + op, *upn = a.upn + op;
     const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1), sn = __ldg(g.sc + j), is = __ldg(g.is_c + j);
-    for (int i = i0; i < i0 + 4 && i < g.nr; ++i) {
+    for (int i = i0; i < i0 + 4 && i <= g.ihi_c; ++i) {
       const double ir = __ldg(g.ir_c + i);
       const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1);
       const double ur0 = 0.5 * (uri[IX<KR>(g, i, j, k)] + urn[IX<KR>(g, i, j, k)]);
@@ -252,8 +252,8 @@ __global__ void k_interp_cc(Geo g, InterpArgs a) {
   const int patch = blockIdx.z / 5, q = blockIdx.z % 5;
   if (e >= a.tab_cc.n) return;
   const int K = (q < 3) ? KC : KR;
-  if (K == KC && i >= g.nr) return;
-  if (K == KR && (i < 1 || i > g.nr - 1)) return;
+  if (K == KC && (i < g.ifr_c0 || i > g.ifr_c1)) return;
+  if (K == KR && (i < g.ifr_f0 || i > g.ifr_f1)) return;
   const long long ps = psize(g, K);
   double* X = a.cc[q];
   const double* donor = X + (1 - patch) * ps;
@@ -272,7 +272,7 @@ __global__ void k_interp_vec(Geo g, InterpArgs a) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   const int patch = blockIdx.z / 2, s = blockIdx.z % 2;
-  if (e >= t.n) return;
+  if (e >= t.n || i < g.ifr_c0 || i > g.ifr_c1) return;
   const double* ut = a.ut[s];
   const double* up = a.up[s];
   const double* dut = ut + (1 - patch) * psize(g, KT);
@@ -294,8 +294,8 @@ __global__ void k_pack_cc(Geo g, InterpArgs a, double* __restrict__ buf) {
   const int i = blockIdx.y, q = blockIdx.z;
   if (e >= a.tab_cc.n) return;
   const int K = (q < 3) ? KC : KR;
-  if (K == KC && i >= g.nr) return;
-  if (K == KR && (i < 1 || i > g.nr - 1)) return;
+  if (K == KC && (i < g.ifr_c0 || i > g.ifr_c1)) return;
+  if (K == KR && (i < g.ifr_f0 || i > g.ifr_f1)) return;
   const int jb = a.tab_cc.jb[e], kb = a.tab_cc.kb[e];
   buf[((long long)q * (g.nr + 1) + i) * a.tab_cc.n + e] = interp16(g, K, a.cc[q], i, jb, kb, a.tab_cc.w + 8LL * e);
 }
@@ -304,8 +304,8 @@ __global__ void k_unpack_cc(Geo g, InterpArgs a, const double* __restrict__ buf)
   const int i = blockIdx.y, q = blockIdx.z;
   if (e >= a.tab_cc.n) return;
   const int K = (q < 3) ? KC : KR;
-  if (K == KC && i >= g.nr) return;
-  if (K == KR && (i < 1 || i > g.nr - 1)) return;
+  if (K == KC && (i < g.ifr_c0 || i > g.ifr_c1)) return;
+  if (K == KR && (i < g.ifr_f0 || i > g.ifr_f1)) return;
   a.cc[q][((long long)i * NTk(g, K) + a.tab_cc.tj[e]) * NPk(g, K) + a.tab_cc.tk[e]] =
       buf[((long long)q * (g.nr + 1) + i) * a.tab_cc.n + e];
 }
@@ -315,7 +315,7 @@ __global__ void k_pack_vec(Geo g, InterpArgs a, double* __restrict__ buf) {
   const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y, s = blockIdx.z;
-  if (e >= t.n) return;
+  if (e >= t.n || i < g.ifr_c0 || i > g.ifr_c1) return;
   const double vt = interp16(g, KT, a.ut[s], i, t.jb_t[e], t.kb_t[e], t.w_t + 8LL * e);
   const double vp = interp16(g, KP, a.up[s], i, t.jb_p[e], t.kb_p[e], t.w_p + 8LL * e);
   buf[((long long)s * g.nr + i) * t.n + e] = t.m0[e] * vt + t.m1[e] * vp;
@@ -325,7 +325,7 @@ __global__ void k_unpack_vec(Geo g, InterpArgs a, const double* __restrict__ buf
   const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y, s = blockIdx.z;
-  if (e >= t.n) return;
+  if (e >= t.n || i < g.ifr_c0 || i > g.ifr_c1) return;
   double* tgt = (KTGT == KT) ? a.ut[s] : a.up[s];
   tgt[((long long)i * NTk(g, KTGT) + t.tj[e]) * NPk(g, KTGT) + t.tk[e]] = buf[((long long)s * g.nr + i) * t.n + e];
 }
@@ -356,7 +356,7 @@ void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st) {
 template <int Q, int S, int IB>
 void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   constexpr int K = kind_of(Q);
-  const int nch = (i_hi<K>(g) - i_lo<K>() + IB) / IB;
+  const int nch = (i_hi<K>(g) - i_lo<K>(g) + IB) / IB;
   const dim3 grid((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, g.npatch * nch);
   k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
 }
@@ -383,7 +383,7 @@ void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t s
 }
 
 int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st) {
-  const int nz = (g.nr + 3) / 4;
+  const int nz = (g.ihi_c - g.ilo_c + 4) / 4;
   dim3 grid((g.np + 127) / 128, g.nt, g.npatch * nz);
   if (s == 1) k_pres<1><<<grid, 128, 0, st>>>(g, a);
   else k_pres<2><<<grid, 128, 0, st>>>(g, a);

@@ -154,8 +154,8 @@ __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, in
   coef<Q, AX, true>(g, A, i, j, k, am, a0, ap);
   double di = 1.0 - th * a0;
   if (AX == 0 && K != KR) {          // antisymmetric wall ghost of the increment (RD23)
-    if (m == 0) di = 1.0 - th * (a0 - am);
-    if (m == n - 1) di = 1.0 - th * (a0 - ap);
+    if (m == 0 && g.wall_lo) di = 1.0 - th * (a0 - am);
+    if (m == n - 1 && g.wall_hi) di = 1.0 - th * (a0 - ap);
   }
   const double inv = frcp(di);
   lo = (m == 0) ? 0.0 : -th * am * inv;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
   double* UP = LO + NL * LP;
   double* RH = UP + NL * LP;
   const int patch = (AX == 2) ? blockIdx.y : blockIdx.z;
-  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>() + 1 : (AX == 1) ? NTk(g, K) - 2 : NPk(g, K) - 2;
+  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : (AX == 1) ? NTk(g, K) - 2 : NPk(g, K) - 2;
   const long long po = patch * psize(g, K);
   const Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
   double* __restrict__ R = a.R + po;
@@ -230,11 +230,11 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
   __shared__ int s_i[AX == 2 ? NL : 1], s_j[AX == 2 ? NL : 1], s_nd[AX == 2 ? NL : 1];
   if (AX == 2) {
     const int nj = NTk(g, K) - 2;
-    nlines = ((K == KR) ? g.nr - 1 : g.nr) * nj;
+    nlines = (i_hi<K>(g) - i_lo<K>(g) + 1) * nj;
     L0 = blockIdx.x * NL;
     if (threadIdx.x < NL) {
       const int L = min(L0 + (int)threadIdx.x, nlines - 1);   // clamped: a ragged tile reads valid nodes
-      const int ii = i_lo<K>() + L / nj, jj = 1 + L % nj;
+      const int ii = i_lo<K>(g) + L / nj, jj = 1 + L % nj;
       s_i[threadIdx.x] = ii;
       s_j[threadIdx.x] = jj;
       s_nd[threadIdx.x] = IX<K>(g, ii, jj, 1);
@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
     L0 = blockIdx.x * NL + 1;             // first k of the tile
     nlines = NPk(g, K) - 2 - L0 + 1;      // lines of this tile that exist (may exceed NL)
     k0 = L0 + min(lt, nlines - 1);
-    if (AX == 0) { i0 = i_lo<K>(); j0 = blockIdx.y + 1; stride = NTk(g, K) * NPk(g, K); }
-    else { i0 = blockIdx.y + i_lo<K>(); j0 = 1; stride = NPk(g, K); }
+    if (AX == 0) { i0 = i_lo<K>(g); j0 = blockIdx.y + 1; stride = NTk(g, K) * NPk(g, K); }
+    else { i0 = blockIdx.y + i_lo<K>(g); j0 = 1; stride = NPk(g, K); }
     nd0 = IX<K>(g, i0, j0, k0);
   }
   const bool lvalid = (AX == 2) || lt < nlines;
@@ -390,10 +390,10 @@ int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatc
   }
   dim3 grid;
   if (AX == 2) {
-    const int nlines = ((K == KR) ? g.nr - 1 : g.nr) * (NTk(g, K) - 2);
+    const int nlines = (i_hi<K>(g) - i_lo<K>(g) + 1) * (NTk(g, K) - 2);
     grid = dim3((nlines + NL - 1) / NL, npatch);
   } else {
-    grid = dim3((NPk(g, K) - 2 + NL - 1) / NL, AX == 0 ? NTk(g, K) - 2 : (K == KR ? g.nr - 1 : g.nr), npatch);
+    grid = dim3((NPk(g, K) - 2 + NL - 1) / NL, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
   }
   k_line<Q, AX, MODE, S, P, M><<<grid, 128, smem, st>>>(g, a, ra);
   return (int)(grid.x * grid.y);
@@ -412,7 +412,7 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
     if (n <= 768) YY_L(32, 24);
     YY_L(32, 36);                                  // n <= 1152 (checked at create)
   } else {
-    const int n = (AX == 0) ? ((K == KR) ? g.nr - 1 : g.nr) : NTk(g, K) - 2;
+    const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
     if (n <= 16) YY_L(4, 4);
     if (n <= 32) YY_L(4, 8);
     if (n <= 64) YY_L(8, 8);

@@ -41,9 +41,9 @@ __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict
   const int nd = IX<K>(g, i, j, k);
   const int sr = NTk(g, K) * NPk(g, K), st = NPk(g, K);
   s.c = __ldg(F + nd);
-  if (K != KR && i == 0) s.xm = 2.0 * __ldg(W + j * NPk(g, K) + k) - s.c;
+  if (K != KR && g.wall_lo && i == g.ilo_c) s.xm = 2.0 * __ldg(W + j * NPk(g, K) + k) - s.c;
   else s.xm = __ldg(F + nd - sr);
-  if (K != KR && i == g.nr - 1) s.xp = 2.0 * __ldg(W + wsize(g, K) + j * NPk(g, K) + k) - s.c;
+  if (K != KR && g.wall_hi && i == g.ihi_c) s.xp = 2.0 * __ldg(W + wsize(g, K) + j * NPk(g, K) + k) - s.c;
   else s.xp = __ldg(F + nd + sr);
   s.ym = __ldg(F + nd - st);
   s.yp = __ldg(F + nd + st);
@@ -67,7 +67,7 @@ __device__ __forceinline__ double applyL(const Geo& g, const Astar& A, int i, in
 
 template <int K>
 __device__ __forceinline__ bool solved(const Geo& g, int i, int j, int k) {
-  return i >= i_lo<K>() && i <= i_hi<K>(g) && j >= 1 && j <= NTk(g, K) - 2 && k >= 1 && k <= NPk(g, K) - 2;
+  return i >= i_lo<K>(g) && i <= i_hi<K>(g) && j >= 1 && j <= NTk(g, K) - 2 && k >= 1 && k <= NPk(g, K) - 2;
 }
 
 // divergence contributions at cell centre (i,j,k) of one patch
