@@ -85,16 +85,21 @@ yy_status yy_create(const yy_grid* g, double R1, double R2, double Pr, double Ra
                     yy_ctx** out);
 
 /* Multi-GPU: one process per GPU, one context per process.
- * world = 2: rank r holds patch r (Yin on rank 0, Yang on rank 1) on CUDA device
- * `device`; every Schwarz iteration the donor rank evaluates the partner's fringe
- * from its own patch (Alg. 1 steps 1/3/7) and the two ranks swap
- * them, and the per-(quantity, patch) norms (RD24), over NCCL point-to-point on
- * the context's stream.  world = 1, rank 0 is yy_create on `device`.  Radial
- * slabs (world 4, 8) are not built: YY_EINVAL.  nccl_id: 128 bytes from
+ * world = 2 nslab (2, 4, 8, 16): rank r holds radial slab r % nslab (nr / nslab
+ * rows, nr divisible by nslab) of patch r / nslab (Yin on ranks 0..nslab-1, Yang
+ * on the others) on CUDA device `device`.  Every Schwarz iteration the donor rank
+ * evaluates the partner's fringe (same slab, other patch) from its own data
+ * (Alg. 1 steps 1/3/7) and they swap it; slab neighbours swap r-halo
+ * rows after every update; the r-factor sweeps are the partitioned
+ * (Schur-complement) solve of P:L477-480 across the slabs of a patch (boundary
+ * rows gathered per patch); the per-(quantity, patch, slab) norms (RD24) are
+ * gathered and summed in fixed order — all over NCCL point-to-point on the
+ * context's stream.  world = 1, rank 0 is yy_create on `device`.  nccl_id: 128 bytes from
  * yy_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
  * Collective semantics: every rank calls the same sequence of yy_step.  NCCL is
  * resolved at run time (libnccl.so.2); missing -> YY_ENCCL.  set/get/wall/source
- * calls accept only the rank's own patch. */
+ * calls accept only the rank's own patch, as full-patch arrays (a slab reads its
+ * rows and halos, get writes back the rows it owns). */
 yy_status yy_create_dist(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
                          int32_t world, int32_t rank, const void* nccl_id, int32_t device, yy_ctx** out);
 yy_status yy_nccl_unique_id(void* out128);

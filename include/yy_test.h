@@ -36,6 +36,17 @@ yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar, const dou
 yy_status yy_create_pair(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
                          yy_ctx** out2);
 
+/* 2 nslab one-patch radial-slab contexts in this process on the current device
+ * (out[r], r = patch * nslab + slab; nr divisible by nslab, nr / nslab >= 4):
+ * the yy_create_dist layout of 2 nslab GPUs — r-halo rows, the partitioned
+ * r-sweep across slabs, the fringe swap between (patch, slab)
+ * and (other patch, slab), the fixed-order norm merge — exchanging by device
+ * copies on one shared stream.  set/get_fields take full-patch arrays (each
+ * slab reads its rows and halos, writes back the rows it owns).  yy_step on
+ * any member advances all. */
+yy_status yy_create_slabs(const yy_grid* g, double R1, double R2, double Pr, double Ra, double dt,
+                          int32_t nslab, yy_ctx** out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@ trap 'rm -rf "$OBJ"' EXIT
 pids=()
 "$NVCC" $FLAGS -c -o "$OBJ/api.o" "$HERE/yy_api.cu" 2> "$OBJ/api.log" & pids+=($!)
 "$NVCC" $FLAGS -c -o "$OBJ/kernels.o" "$HERE/yy_kernels.cu" 2> "$OBJ/kernels.log" & pids+=($!)
+"$NVCC" $FLAGS -c -o "$OBJ/slab.o" "$HERE/yy_slab.cu" 2> "$OBJ/slab.log" & pids+=($!)
 # one wrapper file per quantity: distinct file names give distinct CUDA module
 # ids (TUs compiled from the same file name collide at fatbin registration)
 for q in 0 1 2 3; do

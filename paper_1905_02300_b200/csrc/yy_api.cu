@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -51,14 +52,22 @@ struct yy_ctx {
   // local patch 0 = patch0.  mode 0: both patches here; 1: loopback pair (two
   // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
   int patch0 = 0;
+  int nslab = 1, slab = 0, roff = 0, nr_glob = 0;   // radial slab of the patch (nslab > 1)
   int mode = 0;
-  yy_ctx* peer = nullptr;      // loopback partner
   int world = 1, rank = 0;
   void* nccl = nullptr;        // ncclComm_t
   double* fr_send = nullptr;   // fringe values this patch donates to the partner
   double* fr_recv = nullptr;   // fringe values received for this patch
   long long fr_n = 0;
-  double* peer_red = nullptr;  // the partner's per-(slot, patch) sums
+  // radial slabs: partitioned r-sweep buffers and the gathered norm sums
+  double* V = nullptr;
+  double* W = nullptr;
+  double* IF = nullptr;        // [nlines][6] this slab's boundary rows
+  double* IFall = nullptr;     // [nslab][nlines][6] every slab of the patch
+  double* LH = nullptr;        // [nlines][2]
+  double* gath = nullptr;      // [world][2 + 2 NSLOT] every context's sums
+  int nblk[NSLOT] = {};
+  std::vector<yy_ctx*> group;  // loopback: every context of the shell, index = rank
   double t = 0.0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -330,6 +339,34 @@ yy_status build_tables(yy_ctx* ctx, const HostGeo& h) {
 
 long long fsize(const yy_ctx* ctx, int f) { return psize(ctx->g, FKIND[f]); }
 
+// A context's rows of a field of kind K inside the full-patch host array
+// (global rows = local rows + roff): host rows [g0, g1] <-> local rows [g0 - roff, ..].
+// own_only: the rows this context owns (solved rows plus the wall faces it holds).
+void row_window(const yy_ctx* ctx, int K, bool own_only, int* g0, int* g1) {
+  const Geo& g = ctx->g;
+  const int nrg = ctx->nr_glob + (K == KR);
+  if (own_only && ctx->nslab > 1) {
+    if (K == KR) { *g0 = (g.wall_lo ? g.ilo_f - 1 : g.ilo_f) + ctx->roff; *g1 = (g.wall_hi ? g.ihi_f + 1 : g.ihi_f) + ctx->roff; }
+    else { *g0 = g.ilo_c + ctx->roff; *g1 = g.ihi_c + ctx->roff; }
+    return;
+  }
+  *g0 = std::max(0, ctx->roff);
+  *g1 = std::min(nrg - 1, ctx->roff + NRk(g, K) - 1);
+}
+
+// copy the window of one patch's field between a full-patch host array and the context
+yy_status copy_window(yy_ctx* ctx, int K, double* dev_patch, double* host, bool to_device, bool own_only) {
+  const Geo& g = ctx->g;
+  int g0, g1;
+  row_window(ctx, K, own_only, &g0, &g1);
+  const long long plane = (long long)NTk(g, K) * NPk(g, K);
+  const size_t bytes = (size_t)(g1 - g0 + 1) * plane * sizeof(double);
+  double* d = dev_patch + (long long)(g0 - ctx->roff) * plane;
+  double* hh = host + (long long)g0 * plane;
+  CK(to_device ? cudaMemcpy(d, hh, bytes, cudaMemcpyHostToDevice) : cudaMemcpy(hh, d, bytes, cudaMemcpyDeviceToHost));
+  return YY_OK;
+}
+
 yy_status check_args(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system) {
   if (!ctx) return YY_EINVAL;
   if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
@@ -396,124 +433,6 @@ StaticArgs static_args(yy_ctx* ctx, int q, double tsrc) {
 // factor orders as printed (RD28): first factor solved first
 constexpr int ORDER[4][3] = {{0, 1, 2}, {1, 2, 0}, {2, 0, 1}, {0, 1, 2}};
 
-yy_status solve_quantity(yy_ctx* ctx, int q, int s, int slot, int* nblk) {
-  const Geo& g = ctx->g;
-  const int f = (q == QT) ? FT : (q == QUR ? FUR1 : q == QUT ? FUT1 : FUP1) + (s == 2 ? 3 : 0);
-  ResidArgs r{};
-  r.it = ctx->it[f];
-  r.n = ctx->n[f];
-  const int wf = (q == QT) ? WT : (q == QUR ? -1 : q == QUT ? WUT : WUP);
-  r.wnew = wf >= 0 ? ctx->wl[2][wf] : nullptr;
-  r.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
-  r.ar = ctx->astar[0]; r.at = ctx->astar[1]; r.ap = ctx->astar[2];
-  r.G = ctx->G[f];
-  r.R = ctx->R;
-  r.Tit = ctx->it[FT]; r.Tn = ctx->n[FT];
-  const int o = (s == 2) ? 3 : 0;
-  r.urit = ctx->it[FUR1 + o]; r.urn = ctx->n[FUR1 + o];
-  r.utit = ctx->it[FUT1 + o]; r.utn = ctx->n[FUT1 + o];
-  r.p1it = ctx->it[FP1]; r.p1n = ctx->n[FP1];
-  const std::string rname = std::string("resid_") + QNAME[q] + (q ? (s == 1 ? "1" : "2") : "");
-  if (!ctx->fuse) {
-    ProfScope ps(ctx, kname(rname), 1);
-    launch_resid(g, q, s, r, ctx->st);
-  }
-  SweepArgs w{};
-  w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
-  w.R = ctx->R; w.C = ctx->C; w.psi = ctx->it[f];
-  w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
-  w.maxb = ctx->maxb;
-  for (int a = 0; a < 3; ++a) {
-    const bool fin = (a == 2), first = (a == 0) && ctx->fuse;
-    // fused first sweep: class "sweep_<q>_<ax>+resid_<q><s>"
-    ProfScope ps(ctx, kname(std::string("sweep_") + QNAME[q] + "_" + AXNAME[ORDER[q][a]] + (fin ? "_fin" : "") +
-                            (first ? "+" + rname : "")), 1);
-    const int nb = launch_sweep(g, q, ORDER[q][a], s, first, fin, w, first ? &r : nullptr, g.npatch, ctx->st);
-    if (nb < 0) return fail(ctx, YY_ESTATE, "internal: no sweep kernel for this factor");
-    if (fin) nblk[slot] = nb;
-  }
-  return YY_OK;
-}
-
-// O2-O4 and the walls of one step (per context)
-yy_status step_begin(yy_ctx* ctx) {
-  const Geo& g = ctx->g;
-  const double tau = ctx->dt, t = ctx->t;
-  cudaStream_t st = ctx->st;
-  const int NPT = g.npatch;
-  // wall data at t_{n-1}, t_n, t_{n+1}
-  for (int L = 0; L < 3; ++L) TRY(eval_walls(ctx, L, t + (L - 1) * tau));
-  // O2: a* = 1.5 u2^n - 0.5 u2^{n-1}
-  for (int c = 0; c < 3; ++c) {
-    LinIn in{};
-    in.p[0] = ctx->n[FUR2 + c]; in.c[0] = 1.5;
-    in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
-    ProfScope ps(ctx, "astar", 1);
-    launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
-  }
-  // O3: static right-hand sides
-  for (int q = 0; q < 4; ++q) {
-    StaticArgs a = static_args(ctx, q, t + 0.5 * tau);
-    ProfScope ps(ctx, kname(std::string("static_") + QNAME[q]), 1);
-    launch_static(g, q, a, st);
-  }
-  // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
-  for (int f = 0; f < NF; ++f) {
-    ProfScope ps(ctx, "copy_iterate", 0);
-    CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], NPT * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  }
-  const long long plane = (long long)g.nt * g.np;
-  for (int f : {FUR1, FUR2})
-    for (int p = 0; p < NPT; ++p)
-      for (int w = 0; w < 2; ++w)
-        CK(cudaMemcpyAsync(ctx->it[f] + p * fsize(ctx, f) + (w ? g.nr * plane : 0),
-                           ctx->wl[2][WUR] + (p * 2 + w) * plane, plane * sizeof(double),
-                           cudaMemcpyDeviceToDevice, st));
-  return YY_OK;
-}
-
-InterpArgs interp_args(yy_ctx* ctx) {
-  InterpArgs ia{};
-  ia.cc[0] = ctx->it[FT]; ia.cc[1] = ctx->it[FP1]; ia.cc[2] = ctx->it[FP2];
-  ia.cc[3] = ctx->it[FUR1]; ia.cc[4] = ctx->it[FUR2];
-  ia.ut[0] = ctx->it[FUT1]; ia.ut[1] = ctx->it[FUT2];
-  ia.up[0] = ctx->it[FUP1]; ia.up[1] = ctx->it[FUP2];
-  ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
-  return ia;
-}
-
-// O6-O9 of one Schwarz iteration and the local per-(slot, patch) norms (per context)
-yy_status iter_solve(yy_ctx* ctx) {
-  const Geo& g = ctx->g;
-  cudaStream_t st = ctx->st;
-  ReduceArgs ra{};
-  ra.maxb = ctx->maxb;
-  ra.npatch = g.npatch;
-  ra.patch0 = ctx->patch0;
-  TRY(solve_quantity(ctx, QT, 1, 0, ra.nblk));           // O6
-  for (int s = 1; s <= 2; ++s) {                         // O7 / O9
-    const int base = (s == 1) ? 1 : 5;
-    TRY(solve_quantity(ctx, QUR, s, base + 0, ra.nblk));
-    TRY(solve_quantity(ctx, QUT, s, base + 1, ra.nblk));
-    TRY(solve_quantity(ctx, QUP, s, base + 2, ra.nblk));
-    PresArgs pa{};
-    const int o = (s == 2) ? 3 : 0;
-    pa.urit = ctx->it[FUR1 + o]; pa.urn = ctx->n[FUR1 + o];
-    pa.utit = ctx->it[FUT1 + o]; pa.utn = ctx->n[FUT1 + o];
-    pa.upit = ctx->it[FUP1 + o]; pa.upn = ctx->n[FUP1 + o];
-    pa.pn = ctx->n[s == 1 ? FP1 : FP2];
-    pa.p1it = ctx->it[FP1]; pa.p1n = ctx->n[FP1];
-    pa.pit = ctx->it[s == 1 ? FP1 : FP2];
-    pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
-    pa.maxb = ctx->maxb;
-    ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
-    ra.nblk[base + 3] = launch_pres(g, s, pa, st);
-  }
-  ProfScope ps(ctx, "reduce", 1);
-  launch_reduce_slots(ctx->part, ra, ctx->red, st);      // O10, local patches
-  return YY_OK;
-}
-
 // ---- transports between the contexts of a group --------------
 struct NcclApi {
   bool ok = false;
@@ -559,27 +478,248 @@ NcclApi& nccl_api() {
     if (r_ != ncclSuccess) return fail(ctx, YY_ENCCL, std::string(#call ": ") + nccl_api().GetErrorString(r_)); \
   } while (0)
 
-// exchange `count` doubles: each context's src goes to its partner's dst
-yy_status swap_with_partner(std::vector<yy_ctx*>& cs, double* yy_ctx::*src, double* yy_ctx::*dst, long long count) {
-  for (yy_ctx* ctx : cs) {
-    if (ctx->mode == 1) {
-      CK(cudaMemcpyAsync(ctx->peer->*dst, ctx->*src, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
-    } else if (ctx->mode == 2) {
-      NcclApi& N = nccl_api();
-      ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
-      const int partner = 1 - ctx->rank;
-      NK(N.GroupStart());
-      NK(N.Send(ctx->*src, (size_t)count, ncclFloat64, partner, comm, ctx->st));
-      NK(N.Recv(ctx->*dst, (size_t)count, ncclFloat64, partner, comm, ctx->st));
-      NK(N.GroupEnd());
+// ---- transfers between the contexts of a group ----------------
+// A group is every context of one shell: one context (both patches, or one NCCL
+// rank), or a loopback set in this process.  rank = patch * nslab + slab.
+struct Xfer {
+  int src, dst;                                   // ranks
+  std::function<const double*(yy_ctx*)> sp;       // source buffer on the src context
+  std::function<double*(yy_ctx*)> dp;             // destination buffer on the dst context
+  long long count;
+};
+
+yy_ctx* ctx_of(std::vector<yy_ctx*>& cs, int rank) {
+  for (yy_ctx* c : cs) if (c->rank == rank) return c;
+  return nullptr;
+}
+
+yy_status run_xfers(std::vector<yy_ctx*>& cs, const std::vector<Xfer>& ops) {
+  yy_ctx* ctx = cs[0];
+  if (ctx->mode == 2) {                           // NCCL: this rank's sends and receives, one group call
+    NcclApi& N = nccl_api();
+    ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+    NK(N.GroupStart());
+    for (const Xfer& x : ops) {
+      if (x.src == ctx->rank && x.dst == ctx->rank) continue;
+      if (x.src == ctx->rank) NK(N.Send(x.sp(ctx), (size_t)x.count, ncclFloat64, x.dst, comm, ctx->st));
+      if (x.dst == ctx->rank) NK(N.Recv(x.dp(ctx), (size_t)x.count, ncclFloat64, x.src, comm, ctx->st));
     }
+    NK(N.GroupEnd());
+    for (const Xfer& x : ops)
+      if (x.src == ctx->rank && x.dst == ctx->rank)
+        CK(cudaMemcpyAsync(x.dp(ctx), x.sp(ctx), x.count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+    return YY_OK;
+  }
+  for (const Xfer& x : ops) {                     // loopback: one shared stream, plain copies
+    yy_ctx* a = ctx_of(cs, x.src);
+    yy_ctx* b = ctx_of(cs, x.dst);
+    if (!a || !b) return fail(ctx, YY_ESTATE, "internal: transfer to a context outside the group");
+    CK(cudaMemcpyAsync(x.dp(b), x.sp(a), x.count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
   }
   return YY_OK;
 }
 
-// O5: fringe of every patch from the other patch's iterate k-1
+bool distributed(const std::vector<yy_ctx*>& cs) { return !(cs.size() == 1 && cs[0]->mode == 0); }
+int world_of(const yy_ctx* c) { return 2 * c->nslab; }
+
+// N1: r-halo rows of one iterate field with the slab neighbours of the same patch
+yy_status exchange_halos(std::vector<yy_ctx*>& cs, int f) {
+  yy_ctx* c0 = cs[0];
+  if (c0->nslab == 1) return YY_OK;
+  const Geo& g = c0->g;
+  const int K = FKIND[f], S = c0->nslab, nl = g.ihi_c - g.ilo_c + 1;
+  const long long plane = (long long)NTk(g, K) * NPk(g, K);
+  // owned boundary rows and the neighbour's halo rows (local indices)
+  const int own_lo = (K == KR) ? 2 : 1, own_hi = (K == KR) ? nl + 1 : nl;
+  const int halo_lo = (K == KR) ? 1 : 0, halo_hi = (K == KR) ? nl + 2 : nl + 1;
+  std::vector<Xfer> ops;
+  for (int p = 0; p < 2; ++p)
+    for (int sl = 1; sl < S; ++sl) {
+      const int up = p * S + sl, dn = up - 1;      // slab sl and the one below it
+      ops.push_back({up, dn, [=](yy_ctx* c) -> const double* { return c->it[f] + own_lo * plane; },
+                     [=](yy_ctx* c) { return c->it[f] + halo_hi * plane; }, plane});
+      ops.push_back({dn, up, [=](yy_ctx* c) -> const double* { return c->it[f] + own_hi * plane; },
+                     [=](yy_ctx* c) { return c->it[f] + halo_lo * plane; }, plane});
+    }
+  return run_xfers(cs, ops);
+}
+
+// the quantity's iterate field
+int qfield(int q, int s) { return (q == QT) ? FT : (q == QUR ? FUR1 : q == QUT ? FUT1 : FUP1) + (s == 2 ? 3 : 0); }
+
+ResidArgs resid_args(yy_ctx* ctx, int q, int s) {
+  const int f = qfield(q, s);
+  ResidArgs r{};
+  r.it = ctx->it[f];
+  r.n = ctx->n[f];
+  const int wf = (q == QT) ? WT : (q == QUR ? -1 : q == QUT ? WUT : WUP);
+  r.wnew = wf >= 0 ? ctx->wl[2][wf] : nullptr;
+  r.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
+  r.ar = ctx->astar[0]; r.at = ctx->astar[1]; r.ap = ctx->astar[2];
+  r.G = ctx->G[f];
+  r.R = ctx->R;
+  r.Tit = ctx->it[FT]; r.Tn = ctx->n[FT];
+  const int o = (s == 2) ? 3 : 0;
+  r.urit = ctx->it[FUR1 + o]; r.urn = ctx->n[FUR1 + o];
+  r.utit = ctx->it[FUT1 + o]; r.utn = ctx->n[FUT1 + o];
+  r.p1it = ctx->it[FP1]; r.p1n = ctx->n[FP1];
+  return r;
+}
+
+SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
+  SweepArgs w{};
+  w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
+  w.R = ctx->R; w.psi = ctx->it[qfield(q, s)];
+  w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
+  w.maxb = ctx->maxb;
+  w.V = ctx->V; w.W = ctx->W; w.IF = ctx->IF;
+  return w;
+}
+
+// O6/O7/O9 for one quantity on every context of the group: residual, the three
+// factor sweeps in the printed order (RD28) — the r-factor of radial slabs as the
+// partitioned solve across slabs — and the r-halos of the updated iterate
+yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
+  const std::string rname = std::string("resid_") + QNAME[q] + (q ? (s == 1 ? "1" : "2") : "");
+  for (yy_ctx* ctx : cs) {
+    if (ctx->fuse) continue;
+    ResidArgs r = resid_args(ctx, q, s);
+    ProfScope ps(ctx, kname(rname), 1);
+    launch_resid(ctx->g, q, s, r, ctx->st);
+  }
+  const int S = cs[0]->nslab;
+  for (int a = 0; a < 3; ++a) {
+    const int ax = ORDER[q][a];
+    const bool fin = (a == 2), first = (a == 0) && cs[0]->fuse;
+    const std::string cls = std::string("sweep_") + QNAME[q] + "_" + AXNAME[ax] + (fin ? "_fin" : "") +
+                            (first ? "+" + rname : "");
+    if (ax == 0 && S > 1) {
+      const Geo& g = cs[0]->g;
+      const int K = kind_of(q), nlines = (NTk(g, K) - 2) * (NPk(g, K) - 2);
+      for (yy_ctx* ctx : cs) {
+        SweepArgs w = sweep_args(ctx, q, s, slot);
+        ProfScope ps(ctx, kname(cls + "_slab"), 1);
+        const int nb = launch_sweep(ctx->g, q, ax, s, false, false, true, w, nullptr, 1, ctx->st);
+        if (nb < 0) return fail(ctx, YY_ESTATE, "radial slab lines must fill the line chunks (nr / nslab)");
+      }
+      std::vector<Xfer> ops;                      // N2: boundary rows of every slab to its patch group
+      for (int p = 0; p < 2; ++p)
+        for (int a1 = 0; a1 < S; ++a1)
+          for (int b1 = 0; b1 < S; ++b1)
+            ops.push_back({p * S + a1, p * S + b1, [](yy_ctx* c) -> const double* { return c->IF; },
+                           [=](yy_ctx* c) { return c->IFall + (long long)a1 * nlines * 6; }, 6LL * nlines});
+      TRY(run_xfers(cs, ops));
+      for (yy_ctx* ctx : cs) {
+        SweepArgs w = sweep_args(ctx, q, s, slot);
+        SlabArgs sa{ctx->IFall, ctx->LH, S, ctx->slab, nlines};
+        ProfScope ps(ctx, kname(cls + "_couple"), 2);
+        launch_slab_solve(sa, ctx->st);
+        const int nb = launch_slab_correct(ctx->g, K, fin, w, ctx->LH, ctx->st);
+        if (fin) ctx->nblk[slot] = nb;
+      }
+      continue;
+    }
+    for (yy_ctx* ctx : cs) {
+      ResidArgs r = resid_args(ctx, q, s);
+      SweepArgs w = sweep_args(ctx, q, s, slot);
+      ProfScope ps(ctx, kname(cls), 1);
+      const int nb = launch_sweep(ctx->g, q, ax, s, first, fin, false, w, first ? &r : nullptr, ctx->g.npatch,
+                                  ctx->st);
+      if (nb < 0) return fail(ctx, YY_ESTATE, "internal: no sweep kernel for this factor");
+      if (fin) ctx->nblk[slot] = nb;
+    }
+  }
+  return exchange_halos(cs, qfield(q, s));
+}
+
+// O2-O4 and the walls of one step (per context)
+yy_status step_begin(yy_ctx* ctx) {
+  const Geo& g = ctx->g;
+  const double tau = ctx->dt, t = ctx->t;
+  cudaStream_t st = ctx->st;
+  const int NPT = g.npatch;
+  // wall data at t_{n-1}, t_n, t_{n+1}
+  for (int L = 0; L < 3; ++L) TRY(eval_walls(ctx, L, t + (L - 1) * tau));
+  // O2: a* = 1.5 u2^n - 0.5 u2^{n-1}
+  for (int c = 0; c < 3; ++c) {
+    LinIn in{};
+    in.p[0] = ctx->n[FUR2 + c]; in.c[0] = 1.5;
+    in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
+    ProfScope ps(ctx, "astar", 1);
+    launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
+  }
+  // O3: static right-hand sides
+  for (int q = 0; q < 4; ++q) {
+    StaticArgs a = static_args(ctx, q, t + 0.5 * tau);
+    ProfScope ps(ctx, kname(std::string("static_") + QNAME[q]), 1);
+    launch_static(g, q, a, st);
+  }
+  // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
+  for (int f = 0; f < NF; ++f) {
+    ProfScope ps(ctx, "copy_iterate", 0);
+    CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], NPT * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  const long long plane = (long long)g.nt * g.np;
+  for (int f : {FUR1, FUR2})
+    for (int p = 0; p < NPT; ++p)
+      for (int w = 0; w < 2; ++w)
+        if (w ? g.wall_hi : g.wall_lo)     // wall faces ilo_f - 1 (r = R1), ihi_f + 1 (r = R2)
+          CK(cudaMemcpyAsync(ctx->it[f] + p * fsize(ctx, f) + (long long)(w ? g.ihi_f + 1 : g.ilo_f - 1) * plane,
+                             ctx->wl[2][WUR] + (p * 2 + w) * plane, plane * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st));
+  return YY_OK;
+}
+
+InterpArgs interp_args(yy_ctx* ctx) {
+  InterpArgs ia{};
+  ia.cc[0] = ctx->it[FT]; ia.cc[1] = ctx->it[FP1]; ia.cc[2] = ctx->it[FP2];
+  ia.cc[3] = ctx->it[FUR1]; ia.cc[4] = ctx->it[FUR2];
+  ia.ut[0] = ctx->it[FUT1]; ia.ut[1] = ctx->it[FUT2];
+  ia.up[0] = ctx->it[FUP1]; ia.up[1] = ctx->it[FUP2];
+  ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
+  return ia;
+}
+
+// O6-O9 of one Schwarz iteration on every context of the group and each
+// context's per-(slot, patch) norm sums
+yy_status iter_solve(std::vector<yy_ctx*>& cs) {
+  TRY(solve_quantity(cs, QT, 1, 0));                     // O6
+  for (int s = 1; s <= 2; ++s) {                         // O7 / O9
+    const int base = (s == 1) ? 1 : 5;
+    TRY(solve_quantity(cs, QUR, s, base + 0));
+    TRY(solve_quantity(cs, QUT, s, base + 1));
+    TRY(solve_quantity(cs, QUP, s, base + 2));
+    for (yy_ctx* ctx : cs) {
+      PresArgs pa{};
+      const int o = (s == 2) ? 3 : 0;
+      pa.urit = ctx->it[FUR1 + o]; pa.urn = ctx->n[FUR1 + o];
+      pa.utit = ctx->it[FUT1 + o]; pa.utn = ctx->n[FUT1 + o];
+      pa.upit = ctx->it[FUP1 + o]; pa.upn = ctx->n[FUP1 + o];
+      pa.pn = ctx->n[s == 1 ? FP1 : FP2];
+      pa.p1it = ctx->it[FP1]; pa.p1n = ctx->n[FP1];
+      pa.pit = ctx->it[s == 1 ? FP1 : FP2];
+      pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
+      pa.maxb = ctx->maxb;
+      ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
+      ctx->nblk[base + 3] = launch_pres(ctx->g, s, pa, ctx->st);
+    }
+    TRY(exchange_halos(cs, s == 1 ? FP1 : FP2));
+  }
+  for (yy_ctx* ctx : cs) {
+    ReduceArgs ra{};
+    for (int q = 0; q < NSLOT; ++q) ra.nblk[q] = ctx->nblk[q];
+    ra.maxb = ctx->maxb;
+    ra.npatch = ctx->g.npatch;
+    ra.patch0 = ctx->patch0;
+    ProfScope ps(ctx, "reduce", 1);
+    launch_reduce_slots(ctx->part, ra, ctx->red, ctx->st);   // O10, local patches
+  }
+  return YY_OK;
+}
+
+// O5 (N3): fringe of every patch from the other patch's iterate k-1
 yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
-  if (cs.size() == 1 && cs[0]->mode == 0) {
+  if (!distributed(cs)) {
     yy_ctx* ctx = cs[0];
     ProfScope ps(ctx, "interp", 3);
     launch_interp(ctx->g, interp_args(ctx), ctx->st);
@@ -589,7 +729,13 @@ yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
     ProfScope ps(ctx, "fringe_pack", 3);
     launch_fringe_pack(ctx->g, interp_args(ctx), ctx->fr_send, ctx->st);
   }
-  TRY(swap_with_partner(cs, &yy_ctx::fr_send, &yy_ctx::fr_recv, cs[0]->fr_n));
+  const int S = cs[0]->nslab;
+  const long long n = cs[0]->fr_n;
+  std::vector<Xfer> ops;
+  for (int r = 0; r < 2 * S; ++r)
+    ops.push_back({r, (r + S) % (2 * S), [](yy_ctx* c) -> const double* { return c->fr_send; },
+                   [](yy_ctx* c) { return c->fr_recv; }, n});
+  TRY(run_xfers(cs, ops));
   for (yy_ctx* ctx : cs) {
     ProfScope ps(ctx, "fringe_unpack", 3);
     launch_fringe_unpack(ctx->g, interp_args(ctx), ctx->fr_recv, ctx->st);
@@ -597,11 +743,19 @@ yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
   return YY_OK;
 }
 
-// O10: rho_k from the sums of all patches (fixed order, identical on every context)
+// O10 (N4): rho_k from the sums of all patches and slabs, in fixed order, so that
+// every context computes the same value and takes the same iteration count
 yy_status reduce_group(std::vector<yy_ctx*>& cs) {
-  if (!(cs.size() == 1 && cs[0]->mode == 0)) {
-    TRY(swap_with_partner(cs, &yy_ctx::red, &yy_ctx::peer_red, 2 + 2 * NSLOT));
-    for (yy_ctx* ctx : cs) launch_merge_sums(ctx->red, ctx->peer_red, 1 - ctx->patch0, ctx->st);
+  if (distributed(cs)) {
+    const int W = world_of(cs[0]);
+    const long long m = 2 + 2 * NSLOT;
+    std::vector<Xfer> ops;
+    for (int a = 0; a < W; ++a)
+      for (int b = 0; b < W; ++b)
+        ops.push_back({a, b, [](yy_ctx* c) -> const double* { return c->red; },
+                       [=](yy_ctx* c) { return c->gath + a * m; }, m});
+    TRY(run_xfers(cs, ops));
+    for (yy_ctx* ctx : cs) launch_merge_all(ctx->red, ctx->gath, ctx->nslab, ctx->st);
   }
   for (yy_ctx* ctx : cs) {
     ProfScope ps(ctx, "reduce", 1);
@@ -637,7 +791,7 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   while (k < kmax) {
     ++k;
     TRY(exchange_fringe(cs));                              // O5
-    for (yy_ctx* c : cs) TRY(iter_solve(c));               // O6-O9, local norms
+    TRY(iter_solve(cs));                                   // O6-O9, local norms
     TRY(reduce_group(cs));                                 // O10
     for (yy_ctx* c : cs) {
       yy_ctx* ctx = c;
@@ -668,10 +822,15 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
 // C ABI
 // =====================================================================================
 namespace {
+// npatch local patches starting at global patch0; nslab > 1: radial slab `slab`
+// of nslab equal slabs (nr / nslab rows, plus one halo row on each side)
 yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, int npatch,
-                     int patch0, yy_ctx** out) {
+                     int patch0, yy_ctx** out, int nslab = 1, int slab = 0) {
   if (!out) return YY_EINVAL;
   *out = nullptr;
+  if (nslab < 1 || slab < 0 || slab >= nslab || (nslab > 1 && (npatch != 1 || !gr || gr->nr % nslab ||
+                                                               gr->nr / nslab < 4)))
+    return YY_EINVAL;
   if (!gr || gr->nr < 2 || gr->ntheta < 8 || gr->nphi < 8) return YY_EINVAL;
   // longest lines the register-chunked line solver takes (yy_line.cu)
   if (gr->nr > max_line_len(0) || gr->ntheta - 1 > max_line_len(1) || gr->nphi - 1 > max_line_len(2)) return YY_EINVAL;
@@ -686,9 +845,25 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   g.nr = h.nr; g.nt = h.nt; g.np = h.np;
   g.npatch = npatch;
   ctx->patch0 = patch0;
+  ctx->nslab = nslab;
+  ctx->slab = slab;
+  ctx->nr_glob = h.nr;
   g.ilo_c = 0; g.ihi_c = h.nr - 1; g.ilo_f = 1; g.ihi_f = h.nr - 1;
   g.wall_lo = g.wall_hi = 1;
   g.ifr_c0 = 0; g.ifr_c1 = h.nr - 1; g.ifr_f0 = 1; g.ifr_f1 = h.nr - 1;
+  if (nslab > 1) {
+    // local row i = global row i + roff, roff = slab nl - 1: rows 1..nl owned,
+    // rows 0 and nl+1 halos; local face f = global face f + roff
+    const int nl = h.nr / nslab;
+    ctx->roff = slab * nl - 1;
+    g.nr = nl + 2;
+    g.wall_lo = slab == 0;
+    g.wall_hi = slab == nslab - 1;
+    g.ilo_c = 1; g.ihi_c = nl;
+    g.ilo_f = 2; g.ihi_f = g.wall_hi ? nl : nl + 1;
+    g.ifr_c0 = 0; g.ifr_c1 = nl + 1;
+    g.ifr_f0 = g.wall_lo ? 2 : 1; g.ifr_f1 = g.wall_hi ? nl : nl + 2;
+  }
   g.dr = h.dr; g.dth = h.dth; g.dph = h.dph; g.R1 = R1;
   g.tau = dt; g.nu = Pr; g.kap = 1.0;
   g.cchi = 1.0 / (2.0 * ctx->chi); g.inv_chi = 1.0 / ctx->chi; g.PrRa = Pr * Ra;
@@ -696,11 +871,11 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   g.hatph = 1.0 / (R1 * R1 * std::sin(th1) * std::sin(th1) * h.dph * h.dph);
   // 1-D coordinate and factor tables (SURVEY Appendix A rows as products of
   // 1-D factors; computed once here in fp64, so no kernel divides)
-  const int nr = h.nr, nt = h.nt;
+  const int nr = g.nr, nt = h.nt;   // local rows (a slab's include its halos)
   const double dr = h.dr, dth = h.dth;
   std::vector<double> rc(nr), rf(nr + 1), sc(nt), sf(nt + 1), cc(nt), cf(nt + 1);
-  for (int i = 0; i < nr; ++i) rc[i] = R1 + (i + 0.5) * dr;
-  for (int i = 0; i <= nr; ++i) rf[i] = R1 + i * dr;
+  for (int i = 0; i < nr; ++i) rc[i] = R1 + (i + ctx->roff + 0.5) * dr;
+  for (int i = 0; i <= nr; ++i) rf[i] = R1 + (i + ctx->roff) * dr;
   for (int j = 0; j < nt; ++j) { sc[j] = std::sin(h.th0 + (j + 0.5) * dth); cc[j] = std::cos(h.th0 + (j + 0.5) * dth); }
   for (int j = 0; j <= nt; ++j) { sf[j] = std::sin(h.th0 + j * dth); cf[j] = std::cos(h.th0 + j * dth); }
   std::vector<double> tab;
@@ -791,13 +966,21 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   for (int L = 0; L < 3; ++L)
     for (int f = 0; f < NW; ++f)
       if ((s = dalloc(ctx, &ctx->wl[L][f], 2 * npatch * wsize(g, WKIND[f]))) != YY_OK) { yy_destroy(ctx); return s; }
-  if (npatch == 1) {   // fringe transfer buffers of a one-patch context
+  if (npatch == 1) {   // transfer buffers of a one-patch context
     InterpArgs ia{};
     ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
     ctx->fr_n = fringe_count(g, ia);
     if ((s = dalloc(ctx, &ctx->fr_send, ctx->fr_n)) != YY_OK || (s = dalloc(ctx, &ctx->fr_recv, ctx->fr_n)) != YY_OK ||
-        (s = dalloc(ctx, &ctx->peer_red, 2 + 2 * NSLOT)) != YY_OK) { yy_destroy(ctx); return s; }
+        (s = dalloc(ctx, &ctx->gath, (size_t)2 * nslab * (2 + 2 * NSLOT))) != YY_OK) { yy_destroy(ctx); return s; }
   }
+  if (nslab > 1) {     // partitioned r-sweep buffers
+    long long nlmax = 0;
+    for (int K = 0; K < 4; ++K) nlmax = std::max(nlmax, (long long)(NTk(g, K) - 2) * (NPk(g, K) - 2));
+    if ((s = dalloc(ctx, &ctx->V, maxk)) != YY_OK || (s = dalloc(ctx, &ctx->W, maxk)) != YY_OK ||
+        (s = dalloc(ctx, &ctx->IF, 6 * nlmax)) != YY_OK || (s = dalloc(ctx, &ctx->IFall, 6 * nslab * nlmax)) != YY_OK ||
+        (s = dalloc(ctx, &ctx->LH, 2 * nlmax)) != YY_OK) { yy_destroy(ctx); return s; }
+  }
+  ctx->rank = patch0 * nslab + slab;
   if (cudaDeviceSynchronize() != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
   *out = ctx;
   return YY_OK;
@@ -829,13 +1012,14 @@ yy_status yy_create_dist(const yy_grid* gr, double R1, double R2, double Pr, dou
     if (cudaSetDevice(device) != cudaSuccess) return YY_ECUDA;
     return yy_create(gr, R1, R2, Pr, Ra, dt, out);
   }
-  // one rank per patch (Yin = rank 0, Yang = rank 1); radial slabs (world 4, 8) are not built
-  if (world != 2 || rank < 0 || rank > 1 || !nccl_id) return YY_EINVAL;
+  // world = 2 nslab: rank = patch nslab + slab (Yin on ranks 0..nslab-1, Yang on the rest)
+  if (world < 2 || world % 2 || world > 16 || rank < 0 || rank >= world || !nccl_id) return YY_EINVAL;
+  const int nslab = world / 2;
   NcclApi& N = nccl_api();
   if (!N.ok) return YY_ENCCL;
   if (cudaSetDevice(device) != cudaSuccess) return YY_ECUDA;
   yy_ctx* ctx = nullptr;
-  yy_status s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, rank, &ctx);
+  yy_status s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, rank / nslab, &ctx, nslab, rank % nslab);
   if (s != YY_OK) return s;
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof(id));
@@ -860,9 +1044,29 @@ yy_status yy_create_pair(const yy_grid* gr, double R1, double R2, double Pr, dou
   s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, 1, &out2[1]);
   if (s != YY_OK) { yy_destroy(out2[0]); out2[0] = nullptr; return s; }
   out2[0]->mode = out2[1]->mode = 1;
-  out2[0]->peer = out2[1];
-  out2[1]->peer = out2[0];
+  out2[0]->group = out2[1]->group = {out2[0], out2[1]};
   out2[1]->st = out2[0]->st;
+  return YY_OK;
+}
+
+yy_status yy_create_slabs(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, int32_t nslab,
+                          yy_ctx** out) {
+  if (!out || nslab < 1 || nslab > 8) return YY_EINVAL;
+  std::vector<yy_ctx*> cs(2 * nslab, nullptr);
+  for (int r = 0; r < 2 * nslab; ++r) {
+    out[r] = nullptr;
+    yy_status s = create_ctx(gr, R1, R2, Pr, Ra, dt, 1, r / nslab, &cs[r], nslab, r % nslab);
+    if (s != YY_OK) {
+      for (yy_ctx* c : cs) if (c) { c->group.clear(); yy_destroy(c); }
+      return s;
+    }
+  }
+  for (int r = 0; r < 2 * nslab; ++r) {
+    cs[r]->mode = 1;
+    cs[r]->group = cs;
+    cs[r]->st = cs[0]->st;
+    out[r] = cs[r];
+  }
   return YY_OK;
 }
 
@@ -874,8 +1078,7 @@ yy_status yy_set_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t syste
   auto put = [&](int fidx, const double* src) -> yy_status {
     if (!src) return YY_OK;
     const long long sz = fsize(ctx, fidx);
-    CK(cudaMemcpy(L[fidx] + (patch - ctx->patch0) * sz, src, sz * sizeof(double), cudaMemcpyHostToDevice));
-    return YY_OK;
+    return copy_window(ctx, FKIND[fidx], L[fidx] + (patch - ctx->patch0) * sz, const_cast<double*>(src), true, false);
   };
   for (int s = sys_lo; s <= sys_hi; ++s) {
     const int o = (s == 2) ? 3 : 0;
@@ -895,8 +1098,7 @@ yy_status yy_get_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t syste
   auto get = [&](int fidx, double* dst) -> yy_status {
     if (!dst) return YY_OK;
     const long long sz = fsize(ctx, fidx);
-    CK(cudaMemcpy(dst, L[fidx] + (patch - ctx->patch0) * sz, sz * sizeof(double), cudaMemcpyDeviceToHost));
-    return YY_OK;
+    return copy_window(ctx, FKIND[fidx], L[fidx] + (patch - ctx->patch0) * sz, dst, false, true);
   };
   const int o = (system == 2) ? 3 : 0;
   TRY(get(FUR1 + o, f->ur));
@@ -927,7 +1129,9 @@ static yy_status set_terms(yy_ctx* ctx, int32_t patch, int32_t nterms, const int
       const long long sz = wall ? 2 * wsize(g, WKIND[f]) : psize(g, WKIND[f]);
       double* d = nullptr;
       TRY(dalloc(ctx, &d, sz));
-      CK(cudaMemcpy(d, src[f], sz * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemset(d, 0, sz * sizeof(double)));
+      if (wall) CK(cudaMemcpy(d, src[f], sz * sizeof(double), cudaMemcpyHostToDevice));
+      else TRY(copy_window(ctx, WKIND[f], d, const_cast<double*>(src[f]), true, false));
       slot = d;
     }
     (wall ? ctx->wtf : ctx->stf)[patch][m] = timefn[m];
@@ -974,7 +1178,8 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
 yy_status yy_set_stream(yy_ctx* ctx, void* stream) {
   if (!ctx) return YY_EINVAL;
   ctx->st = static_cast<cudaStream_t>(stream);
-  if (ctx->mode == 1 && ctx->peer) ctx->peer->st = ctx->st;   // a loopback pair shares one stream
+  if (ctx->mode == 1)   // a loopback group shares one stream
+    for (yy_ctx* c : ctx->group) if (c) c->st = ctx->st;
   return YY_OK;
 }
 
@@ -985,9 +1190,11 @@ yy_status yy_step(yy_ctx* ctx, int32_t nsteps, double tol) {
   // the group that holds both patches: this context, or a loopback pair (Yin first)
   std::vector<yy_ctx*> cs{ctx};
   if (ctx->mode == 1) {
-    if (!ctx->peer) return fail(ctx, YY_ESTATE, "loopback partner destroyed");
-    if (ctx->peer->dead) return fail(ctx, YY_ESTATE, "loopback partner unusable");
-    cs = ctx->patch0 == 0 ? std::vector<yy_ctx*>{ctx, ctx->peer} : std::vector<yy_ctx*>{ctx->peer, ctx};
+    cs = ctx->group;
+    for (yy_ctx* c : cs) {
+      if (!c) return fail(ctx, YY_ESTATE, "loopback group member destroyed");
+      if (c->dead) return fail(ctx, YY_ESTATE, "loopback group member unusable");
+    }
   }
   yy_status res = YY_OK;
   for (int s = 0; s < nsteps; ++s) {
@@ -1041,7 +1248,10 @@ const char* yy_last_error(const yy_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 
 void yy_destroy(yy_ctx* ctx) {
   if (!ctx) return;
-  if (ctx->mode == 1 && ctx->peer) ctx->peer->peer = nullptr;
+  if (ctx->mode == 1)
+    for (yy_ctx* c : ctx->group)
+      if (c && c != ctx)
+        for (auto& m : c->group) if (m == ctx) m = nullptr;
   if (ctx->mode == 2 && ctx->nccl) nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->nccl));
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->red_host) cudaFreeHost(ctx->red_host);
@@ -1075,7 +1285,7 @@ extern "C" yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar
   SweepArgs w{};
   w.ar = d_ar; w.at = d_at; w.ap = d_ap;
   w.R = d_x; w.C = ctx->C; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
-  launch_sweep(ctx->g, QT, axis, 1, false, false, w, nullptr, 1, ctx->st);
+  launch_sweep(ctx->g, QT, axis, 1, false, false, false, w, nullptr, 1, ctx->st);
   CK(cudaGetLastError());
   return YY_OK;
 }

@@ -48,11 +48,24 @@ struct ResidArgs {
 
 struct SweepArgs {
   const double *ar, *at, *ap;
-  double* R;                 // in: rhs, out: solution (non-final)
-  double* C;                 // c' scratch
+  double* R;                 // in: rhs, out: solution (non-final); slab r-sweep: x0
+  double* C;                 // unused
   double* psi;               // FINAL: psi += x
   double* part;              // FINAL: norm partials of this slot (2 * maxb)
   int maxb;
+  // radial slab r-sweep (partitioned across slabs): responses of the
+  // line to the lower / upper neighbour slab's boundary unknowns, and the per-line
+  // boundary values (x0, xlo, xhi at the first row, then at the last row)
+  double* V;
+  double* W;
+  double* IF;                // [line][6], line = (j-1)(np_k-2) + (k-1)
+};
+
+// one r-line's slab-coupling solution (yy_slab.cu)
+struct SlabArgs {
+  const double* IFall;       // [nslab][nlines][6] boundary values of every slab of the patch
+  double* LH;                // [nlines][2]: this slab's lower / upper neighbour unknowns
+  int nslab, slab, nlines;
 };
 
 struct PresArgs {
@@ -101,17 +114,19 @@ inline int max_line_len(int ax) { return ax == 2 ? 32 * 36 : 32 * 16; }   // unk
 // eq:er residual from *ra (the quantity's first factor), fin = psi += x and the
 // norm partial (its last factor); neither = plain.  Returns blocks launched
 // (norm partial count) or -1 if (ax, first, fin) is not a factor position of Q.
+// slab = the r-factor of a radial slab (partitioned across slabs: writes x0, V, W,
+// IF; finished by launch_slab_solve / launch_slab_correct).
 template <int Q>
-int launch_sweep_q(const Geo& g, int ax, int s, bool first, bool fin, const SweepArgs& a, const ResidArgs* ra,
-                   int npatch, cudaStream_t st);
+int launch_sweep_q(const Geo& g, int ax, int s, bool first, bool fin, bool slab, const SweepArgs& a,
+                   const ResidArgs* ra, int npatch, cudaStream_t st);
 #ifndef YY_LINE_Q   // (the per-quantity line TUs instantiate only their own Q)
-inline int launch_sweep(const Geo& g, int q, int ax, int s, bool first, bool fin, const SweepArgs& a,
+inline int launch_sweep(const Geo& g, int q, int ax, int s, bool first, bool fin, bool slab, const SweepArgs& a,
                         const ResidArgs* ra, int npatch, cudaStream_t st) {
   switch (q) {
-    case 0: return launch_sweep_q<0>(g, ax, s, first, fin, a, ra, npatch, st);
-    case 1: return launch_sweep_q<1>(g, ax, s, first, fin, a, ra, npatch, st);
-    case 2: return launch_sweep_q<2>(g, ax, s, first, fin, a, ra, npatch, st);
-    default: return launch_sweep_q<3>(g, ax, s, first, fin, a, ra, npatch, st);
+    case 0: return launch_sweep_q<0>(g, ax, s, first, fin, slab, a, ra, npatch, st);
+    case 1: return launch_sweep_q<1>(g, ax, s, first, fin, slab, a, ra, npatch, st);
+    case 2: return launch_sweep_q<2>(g, ax, s, first, fin, slab, a, ra, npatch, st);
+    default: return launch_sweep_q<3>(g, ax, s, first, fin, slab, a, ra, npatch, st);
   }
 }
 #endif
@@ -127,7 +142,11 @@ void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st);
 long long fringe_count(const Geo& g, const InterpArgs& a);
 void launch_fringe_pack(const Geo& g, const InterpArgs& a, double* buf, cudaStream_t st);
 void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, cudaStream_t st);
-// out[2 + 2 slot + peer_patch] <- peer[2 + 2 slot + peer_patch] (the partner's sums)
-void launch_merge_sums(double* out, const double* peer, int peer_patch, cudaStream_t st);
+// out[2 + 2 slot + p] <- sum over slabs s (fixed order) of gath[p * nslab + s][2 + 2 slot + p]
+// (gath: every context's sums, world = 2 nslab contexts ordered rank = patch nslab + slab)
+void launch_merge_all(double* out, const double* gath, int nslab, cudaStream_t st);
+// slab r-sweeps: solve the 2 nslab boundary system of every line, then x = x0 + xlo X_LO + xhi X_HI
+void launch_slab_solve(const SlabArgs& a, cudaStream_t st);
+int launch_slab_correct(const Geo& g, int kind, bool fin, const SweepArgs& w, const double* LH, cudaStream_t st);
 
 }  // namespace yy

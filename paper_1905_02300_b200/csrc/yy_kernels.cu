@@ -207,9 +207,6 @@ __global__ void __launch_bounds__(256) k_reduce_slots(const double* __restrict__
   if (threadIdx.x == 0) out[2 + 2 * slot + lp + a.patch0] = t;
 }
 
-__global__ void k_merge_sums(double* __restrict__ out, const double* __restrict__ peer, int pp) {
-  if (threadIdx.x < NSLOT) out[2 + 2 * threadIdx.x + pp] = peer[2 + 2 * threadIdx.x + pp];
-}
 
 __global__ void k_reduce_final(double* __restrict__ out) {
   if (threadIdx.x == 0) {
@@ -422,8 +419,5 @@ void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, 
   if (a.tab_ph.n) k_unpack_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bph);
 }
 
-void launch_merge_sums(double* out, const double* peer, int peer_patch, cudaStream_t st) {
-  k_merge_sums<<<1, 32, 0, st>>>(out, peer, peer_patch);
-}
 
 }  // namespace yy

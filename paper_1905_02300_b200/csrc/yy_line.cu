@@ -144,10 +144,100 @@ __device__ __forceinline__ void prefetch_rows(const Geo& g, const Astar& A, int 
   }
 }
 
+// part_solve for a line that is one radial slab of a longer r-line (SURVEY
+// §8(e)): row 0 couples (lo_0) to the unknown last row x_lo of the slab below and
+// row n-1 = P M - 1 couples (up_{n-1}) to the unknown first row x_hi of the slab
+// above.  Returns, per row, x = x0 + xl x_lo + xh x_hi (x0 in rh, xl in lo, xh in
+// up): the same elimination, two more right-hand-side columns in the interface
+// PCR (the external couplings moved to the right-hand side).  keep_hi requires
+// the line to fill the chunks exactly (no identity rows).
+template <int P, int M>
+__device__ __forceinline__ void part_solve3(double (&lo)[M], double (&up)[M], double (&rh)[M], int c) {
+  double cp = 0.0, yp = 0.0, vp = 0.0;
+#pragma unroll
+  for (int t = 0; t < M - 1; ++t) {
+    const double l = lo[t];
+    if (t == 0) {
+      cp = up[0];
+      yp = rh[0];
+      vp = -l;
+    } else {
+      const double inv = frcp(1.0 - l * cp);
+      cp = up[t] * inv;
+      yp = (rh[t] - l * yp) * inv;
+      vp = -l * vp * inv;
+    }
+    up[t] = cp;
+    rh[t] = yp;
+    lo[t] = vp;
+  }
+  {
+    double y = rh[M - 2], v = lo[M - 2], w = -up[M - 2];
+    up[M - 2] = w;
+#pragma unroll
+    for (int t = M - 3; t >= 0; --t) {
+      const double ct = up[t];
+      y = rh[t] - ct * y;
+      v = lo[t] - ct * v;
+      w = -ct * w;
+      rh[t] = y;
+      lo[t] = v;
+      up[t] = w;
+    }
+  }
+  const double Y0n = __shfl_down_sync(FULL, rh[0], 1, P);
+  const double V0n = __shfl_down_sync(FULL, lo[0], 1, P);
+  const double W0n = __shfl_down_sync(FULL, up[0], 1, P);
+  const double ae = lo[M - 1], ce = up[M - 1];
+  const bool last = (c == P - 1);
+  double A = ae * lo[M - 2];
+  double B = ae * up[M - 2] + 1.0 + (last ? 0.0 : ce * V0n);
+  double C = last ? 0.0 : ce * W0n;
+  double D = rh[M - 1] - ae * rh[M - 2] - (last ? 0.0 : ce * Y0n);
+  double Dl = 0.0, Dh = last ? -ce : 0.0;     // x_hi enters the last row through ce
+  if (c == 0) {                               // x_lo enters chunk 0 through v (g_{-1})
+    Dl = -A;
+    A = 0.0;
+  }
+#pragma unroll
+  for (int s = 1; s < P; s <<= 1) {
+    const double iB = frcp(B);
+    const double Am = __shfl_up_sync(FULL, A, s, P), iBm = __shfl_up_sync(FULL, iB, s, P);
+    const double Cm = __shfl_up_sync(FULL, C, s, P), Dm = __shfl_up_sync(FULL, D, s, P);
+    const double Dlm = __shfl_up_sync(FULL, Dl, s, P), Dhm = __shfl_up_sync(FULL, Dh, s, P);
+    const double Ap = __shfl_down_sync(FULL, A, s, P), iBp = __shfl_down_sync(FULL, iB, s, P);
+    const double Cp = __shfl_down_sync(FULL, C, s, P), Dp = __shfl_down_sync(FULL, D, s, P);
+    const double Dlp = __shfl_down_sync(FULL, Dl, s, P), Dhp = __shfl_down_sync(FULL, Dh, s, P);
+    const double al = -A * iBm;
+    const double ga = -C * iBp;
+    B = B + al * Cm + ga * Ap;
+    D = D + al * Dm + ga * Dp;
+    Dl = Dl + al * Dlm + ga * Dlp;
+    Dh = Dh + al * Dhm + ga * Dhp;
+    A = al * Am;
+    C = ga * Cp;
+  }
+  const double iB = frcp(B);
+  const double g0 = D * iB, gl = Dl * iB, gh = Dh * iB;
+  const double g0p = __shfl_up_sync(FULL, g0, 1, P), glp = __shfl_up_sync(FULL, gl, 1, P);
+  const double ghp = __shfl_up_sync(FULL, gh, 1, P);
+  const double g0m = c ? g0p : 0.0, glm = c ? glp : 1.0, ghm = c ? ghp : 0.0;   // g_{-1} = x_lo
+#pragma unroll
+  for (int t = 0; t < M - 1; ++t) {
+    const double v = lo[t], w = up[t];
+    rh[t] = rh[t] + v * g0m + w * g0;
+    lo[t] = v * glm + w * gl;
+    up[t] = v * ghm + w * gh;
+  }
+  rh[M - 1] = g0;
+  lo[M - 1] = gl;
+  up[M - 1] = gh;
+}
+
 // normalised row m (0..n-1) of the factor at node (i,j,k); rv = right-hand side
 template <int Q, int AX>
 __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, int j, int k, int m, int n,
-                                         double rv, double& lo, double& up, double& rh) {
+                                         double rv, double& lo, double& up, double& rh, bool keep_ends = false) {
   constexpr int K = kind_of(Q);
   const double th = 0.5 * g.tau;
   double am, a0, ap;
@@ -158,8 +248,11 @@ __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, in
     if (m == n - 1 && g.wall_hi) di = 1.0 - th * (a0 - ap);
   }
   const double inv = frcp(di);
-  lo = (m == 0) ? 0.0 : -th * am * inv;
-  up = (m == n - 1) ? 0.0 : -th * ap * inv;
+  // line ends: homogeneous Dirichlet increment (fringe, u_r walls) — except the
+  // ends of a radial slab that continue in the neighbour slab (keep_ends)
+  const bool klo = keep_ends && AX == 0 && !g.wall_lo, khi = keep_ends && AX == 0 && !g.wall_hi;
+  lo = (m == 0 && !klo) ? 0.0 : -th * am * inv;
+  up = (m == n - 1 && !khi) ? 0.0 : -th * ap * inv;
   rh = rv * inv;
 }
 
@@ -193,7 +286,7 @@ __host__ __device__ constexpr int line_pitch() {
 // 2.-3. thread (line q / P, chunk q % P) solves its chunk in registers;
 // 4. write back with the build mapping (FINAL: psi += x and the norm partial).
 // ---------------------------------------------------------------------------------
-enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2 };
+enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2, MODE_SLAB = 3 };
 
 // resident 128-thread blocks per SM the register allocation must allow (the
 // chunk arrays are 6 M registers): measured on B200 (C3), 96 registers for
@@ -310,7 +403,7 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
       const int ec = min(e, n - 1);
       node(l, ec, i, j, k);
       double lo, up, rh;
-      make_row<Q, AX>(g, A, i, j, k, ec, n, rv[u], lo, up, rh);
+      make_row<Q, AX>(g, A, i, j, k, ec, n, rv[u], lo, up, rh, MODE == MODE_SLAB);
       const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
       const int s = slot(l, e);
       LO[s] = lo * mk;
@@ -330,9 +423,19 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
       up[u] = UP[o + u];
       rh[u] = RH[o + u];
     }
-    part_solve<P, M>(lo, up, rh, c);
+    if (MODE == MODE_SLAB) {
+      part_solve3<P, M>(lo, up, rh, c);
 #pragma unroll
-    for (int u = 0; u < M; ++u) RH[o + u] = rh[u];
+      for (int u = 0; u < M; ++u) {
+        RH[o + u] = rh[u];
+        LO[o + u] = lo[u];
+        UP[o + u] = up[u];
+      }
+    } else {
+      part_solve<P, M>(lo, up, rh, c);
+#pragma unroll
+      for (int u = 0; u < M; ++u) RH[o + u] = rh[u];
+    }
   }
   __syncthreads();
   // 4. write back
@@ -357,6 +460,17 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
         a.psi[po + nd] = pv[u] + x;
         const double r = rnode<K>(g, i), s = snode<K>(g, j);
         wsum += r * r * s * x * x;
+      } else if (MODE == MODE_SLAB) {
+        const double xl = LO[slot(l, e)], xh = UP[slot(l, e)];
+        R[nd] = x;
+        a.V[po + nd] = xl;
+        a.W[po + nd] = xh;
+        if (e == 0 || e == n - 1) {           // this slab's boundary rows of the line
+          double* f = a.IF + 6LL * ((j - 1) * (NPk(g, K) - 2) + (k - 1)) + (e == 0 ? 0 : 3);
+          f[0] = x;
+          f[1] = xl;
+          f[2] = xh;
+        }
       } else {
         R[nd] = x;
       }
@@ -382,6 +496,8 @@ template <int Q, int AX, int MODE, int S, int P, int M>
 int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   constexpr int NL = 128 / P;
+  // a slab line continued by the slab above must fill its chunks exactly (part_solve3)
+  if (MODE == MODE_SLAB && !g.wall_hi && P * M != i_hi<K>(g) - i_lo<K>(g) + 1) return -2;
   const size_t smem = (size_t)3 * NL * line_pitch<P, (M | 1)>() * sizeof(double);
   static bool attr = false;
   if (!attr && smem > 48 * 1024) {
@@ -430,9 +546,12 @@ constexpr int FIRST_AX[4] = {0, 1, 2, 0};
 constexpr int LAST_AX[4] = {2, 0, 1, 2};
 
 template <int Q, int AX>
-int sweep_axis(const Geo& g, int s, bool first, bool fin, const SweepArgs& a, const ResidArgs* ra, int npatch,
-               cudaStream_t st) {
+int sweep_axis(const Geo& g, int s, bool first, bool fin, bool slab, const SweepArgs& a, const ResidArgs* ra,
+               int npatch, cudaStream_t st) {
   const ResidArgs none{};
+  if constexpr (AX == 0) {
+    if (slab) return first ? -1 : sweep_line<Q, 0, MODE_SLAB, 1>(g, a, none, npatch, st);
+  }
   if constexpr (AX == LAST_AX[Q]) {
     if (fin) return sweep_line<Q, AX, MODE_FINAL, 1>(g, a, none, npatch, st);
   }
@@ -450,18 +569,18 @@ int sweep_axis(const Geo& g, int s, bool first, bool fin, const SweepArgs& a, co
 
 
 template <int Q>
-int launch_sweep_q(const Geo& g, int ax, int s, bool first, bool fin, const SweepArgs& a, const ResidArgs* ra,
-                   int npatch, cudaStream_t st) {
-  if (ax == 0) return sweep_axis<Q, 0>(g, s, first, fin, a, ra, npatch, st);
-  if (ax == 1) return sweep_axis<Q, 1>(g, s, first, fin, a, ra, npatch, st);
-  return sweep_axis<Q, 2>(g, s, first, fin, a, ra, npatch, st);
+int launch_sweep_q(const Geo& g, int ax, int s, bool first, bool fin, bool slab, const SweepArgs& a,
+                   const ResidArgs* ra, int npatch, cudaStream_t st) {
+  if (ax == 0) return sweep_axis<Q, 0>(g, s, first, fin, slab, a, ra, npatch, st);
+  if (ax == 1) return sweep_axis<Q, 1>(g, s, first, fin, slab, a, ra, npatch, st);
+  return sweep_axis<Q, 2>(g, s, first, fin, slab, a, ra, npatch, st);
 }
 
 // one translation unit per quantity (csrc/build.sh compiles this file with
 // -DYY_LINE_Q=0..3 in parallel)
 #ifdef YY_LINE_Q
-template int launch_sweep_q<YY_LINE_Q>(const Geo&, int, int, bool, bool, const SweepArgs&, const ResidArgs*, int,
-                                       cudaStream_t);
+template int launch_sweep_q<YY_LINE_Q>(const Geo&, int, int, bool, bool, bool, const SweepArgs&, const ResidArgs*,
+                                       int, cudaStream_t);
 #endif
 
 }  // namespace yy

@@ -78,10 +78,12 @@ def load_library():
     L.yy_launch_count.restype = ctypes.c_int64
     L.yy_profile_report.argtypes = [ctx, ctypes.c_char_p, c_int32]
     L.yy_create_pair.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double, c_void_p]
+    L.yy_create_slabs.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double, c_int32,
+                                  c_void_p]
     L.yy_create_dist.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double,
                                  c_int32, c_int32, c_void_p, c_int32, POINTER(ctx)]
     L.yy_nccl_unique_id.argtypes = [c_void_p]
-    for name in ("yy_create_pair", "yy_create_dist", "yy_nccl_unique_id", "yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
+    for name in ("yy_create_pair", "yy_create_slabs", "yy_create_dist", "yy_nccl_unique_id", "yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
                  "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve",
                  "yy_profile_report"):
         getattr(L, name).restype = c_int32
@@ -129,6 +131,22 @@ class Shell:
         if st != YY_OK:
             raise YYError(f"yy_create_pair failed with status {st}")
         out = [cls(nr, ntheta, nphi, _handle=c_void_p(hs[p]), _patches=(p,)) for p in range(2)]
+        for sh in out:
+            sh._configure(**kw)
+        return out
+
+    @classmethod
+    def slabs(cls, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3, nslab=2, **kw):
+        """yy_create_slabs (include/yy_test.h): 2*nslab radial-slab contexts
+        [rank = patch*nslab + slab] on this device exchanging through device
+        copies — the yy_create_dist layout of 2*nslab GPUs."""
+        L = load_library()
+        g = yy_grid(nr, ntheta, nphi)
+        hs = (c_void_p * (2 * nslab))()
+        st = L.yy_create_slabs(ctypes.byref(g), R1, R2, Pr, Ra, dt, nslab, hs)
+        if st != YY_OK:
+            raise YYError(f"yy_create_slabs failed with status {st}")
+        out = [cls(nr, ntheta, nphi, _handle=c_void_p(hs[r]), _patches=(r // nslab,)) for r in range(2 * nslab)]
         for sh in out:
             sh._configure(**kw)
         return out
@@ -204,8 +222,11 @@ class Shell:
         f, keep = self._fields(arrays, self.shape)
         self._check(self.L.yy_set_fields(self.h, patch, level, system, ctypes.byref(f)), "yy_set_fields")
 
-    def get_fields(self, patch, level=0, system=2, names=("ur", "ut", "up", "p", "T")):
-        out = {n: np.empty(self.shape(n)) for n in names if not (n == "p" and level == 1)}
+    def get_fields(self, patch, level=0, system=2, names=("ur", "ut", "up", "p", "T"), out=None):
+        """out: optional dict of full-patch arrays to fill (a radial slab writes the
+        rows it owns, so passing the same dict to every slab assembles the patch)."""
+        if out is None:
+            out = {n: np.empty(self.shape(n)) for n in names if not (n == "p" and level == 1)}
         f = yy_fields()
         for n, a in out.items():
             setattr(f, n, _ptr(a))
