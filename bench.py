@@ -224,14 +224,7 @@ def run_yy(args):
     from paper_1905_02300_b200 import Shell
 
     rank, world, local = dist_env()
-    if world > 2:
-        if rank == 0:
-            emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                  "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                  "dtype": "f64", "data": "synthetic", "config": {"workload": args.workload},
-                  "error": "radial slabs (4/8 GPUs, partitioned r-solve) not built; N=1 and N=2 (one patch per GPU) are"})
-        return 0
-    if world == 2:
+    if world > 1:
         return run_yy_dist(args, rank, world, local)
     torch.cuda.set_device(local)
     cfg = W.config(args.workload)
@@ -365,8 +358,9 @@ def run_yy(args):
 
 
 def run_yy_dist(args, rank, world, local):
-    """N = 2: one patch per GPU (yy_create_dist over NCCL).  The workload is the
-    N = 1 one, so total work is fixed: "scaling": "strong"."""
+    """N = 2 nslab GPUs (yy_create_dist over NCCL): rank = patch * nslab + slab,
+    radial slabs of nr / nslab rows.  The workload is the N = 1 one, so the total
+    work is fixed: "scaling": "strong"."""
     import torch
     import torch.distributed as td
 
@@ -379,6 +373,7 @@ def run_yy_dist(args, rank, world, local):
     cfg = W.config(args.workload)
     wl = W.make_workload(cfg)
     stream = torch.cuda.Stream()
+    dist.plan(world, rank, cfg.nr)                 # validates the slab split
     sh = Shell.dist(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, world, rank, uid, local,
                     stream=stream.cuda_stream)
     sh.load_workload(wl)
@@ -411,7 +406,9 @@ def run_yy_dist(args, rank, world, local):
               "steps": args.steps, "warmup": W_, "ms_per_step": ms / args.steps, "higher_is_better": True,
               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
               "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
-                         "parallelism": "one patch per GPU (Yin rank 0, Yang rank 1), NCCL fringe + norm swap",
+                         "parallelism": f"Yin on ranks 0..{world // 2 - 1}, Yang on the others, "
+                                        f"{world // 2} radial slab(s) per patch; NCCL p2p fringe, halos, "
+                                        "slab r-solve interfaces, norms",
                          "schwarz_iters_per_step": Ks,
                          "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
                                            "frac_of_8TBs_per_gpu": model_bytes / (world * HBM_NOMINAL_GBS * 1e9)

@@ -541,6 +541,21 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
 #undef YY_L
 }
 
+// radial-slab r-lines continued by the slab above must fill their chunks exactly
+// (part_solve3): pick P x M = n from this menu
+template <int Q>
+int sweep_slab(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  const ResidArgs none{};
+  const int n = i_hi<K>(g) - i_lo<K>(g) + 1;
+#define YY_S(P_, M_) if (n <= (P_) * (M_) && (g.wall_hi || n == (P_) * (M_))) \
+    return launch_line<Q, 0, MODE_SLAB, 1, P_, M_>(g, a, none, npatch, st);
+  YY_S(4, 4) YY_S(4, 6) YY_S(4, 8) YY_S(8, 6) YY_S(8, 8) YY_S(16, 6) YY_S(16, 8) YY_S(16, 12) YY_S(32, 8)
+  YY_S(32, 12) YY_S(32, 16)
+#undef YY_S
+  return -2;
+}
+
 // factor orders (RD28): T r,th,ph; u_r th,ph,r; u_th ph,r,th; u_ph r,th,ph
 constexpr int FIRST_AX[4] = {0, 1, 2, 0};
 constexpr int LAST_AX[4] = {2, 0, 1, 2};
@@ -550,7 +565,7 @@ int sweep_axis(const Geo& g, int s, bool first, bool fin, bool slab, const Sweep
                int npatch, cudaStream_t st) {
   const ResidArgs none{};
   if constexpr (AX == 0) {
-    if (slab) return first ? -1 : sweep_line<Q, 0, MODE_SLAB, 1>(g, a, none, npatch, st);
+    if (slab) return first ? -1 : sweep_slab<Q>(g, a, npatch, st);
   }
   if constexpr (AX == LAST_AX[Q]) {
     if (fin) return sweep_line<Q, AX, MODE_FINAL, 1>(g, a, none, npatch, st);

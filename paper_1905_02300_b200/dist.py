@@ -2,29 +2,39 @@
 holds, and the NCCL unique id handshake for ``yy_create_dist``.
 
 One process per GPU.  World 1: both patches on the one GPU (``yy_create``).
-World 2: rank r holds patch r (Yin = 0, Yang = 1); the Yin<->Yang fringe
-exchange (Alg. 1 steps 1/3/7) and the per-(quantity, patch) norms
-(RD24) are swapped pairwise over NCCL inside ``yy_step``.  Radial slabs
-(worlds 4 and 8, partitioned r-solve P:L477-480) are not built.
+World 2*nslab: rank r holds radial slab r % nslab of patch r // nslab (Yin on
+the first nslab ranks); inside ``yy_step`` the Yin<->Yang fringe (P:L481-483,
+Alg. 1 steps 1/3/7) is swapped with the same slab of the other patch, r-halo rows
+with the slab neighbours, the boundary rows of the partitioned r-solve
+within the patch, and the per-(quantity, patch, slab) norms (RD24) with everyone,
+over NCCL point-to-point.
 
 ``torch.distributed`` is used only to move the 128-byte id from rank 0 to the
 partner (any backend: gloo moves it through host memory, nccl through the GPU).
 """
 from __future__ import annotations
 
-SUPPORTED_WORLDS = (1, 2)
+SUPPORTED_WORLDS = (1, 2, 4, 8, 16)
 
 
-def plan(world: int, rank: int) -> dict:
-    """{'patches': (...), 'partner': rank or None} for this rank."""
+def plan(world: int, rank: int, nr: int | None = None) -> dict:
+    """This rank's part of the shell: patch, radial slab, and the ranks it talks to
+    (fringe partner = same slab of the other patch; slab neighbours below/above).
+    world = 1: both patches, no partners.  nr (cells per patch, optional) is
+    checked for the slab split."""
     if world not in SUPPORTED_WORLDS:
-        raise ValueError(f"world {world}: only 1 (both patches) or 2 (one patch per rank) is built; "
-                         "radial slabs for 4/8 GPUs are not")
+        raise ValueError(f"world {world}: 1 (both patches) or 2*nslab ranks (nslab = 1, 2, 4, 8)")
     if not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside world {world}")
     if world == 1:
-        return {"patches": (0, 1), "partner": None}
-    return {"patches": (rank,), "partner": 1 - rank}
+        return {"patches": (0, 1), "patch": None, "slab": 0, "nslab": 1, "partner": None,
+                "below": None, "above": None}
+    S = world // 2
+    if nr is not None and (nr % S or nr // S < 4):
+        raise ValueError(f"nr = {nr} does not split into {S} radial slabs of >= 4 rows")
+    p, sl = divmod(rank, S)
+    return {"patches": (p,), "patch": p, "slab": sl, "nslab": S, "partner": (1 - p) * S + sl,
+            "below": rank - 1 if sl > 0 else None, "above": rank + 1 if sl < S - 1 else None}
 
 
 def share_unique_id(rank: int, device=None) -> bytes:

@@ -161,7 +161,7 @@ class Shell:
         st = L.yy_create_dist(ctypes.byref(g), R1, R2, Pr, Ra, dt, world, rank, idb, device, ctypes.byref(h))
         if st != YY_OK:
             raise YYError(f"yy_create_dist failed with status {st}")
-        sh = cls(nr, ntheta, nphi, _handle=h, _patches=(rank,) if world == 2 else (0, 1))
+        sh = cls(nr, ntheta, nphi, _handle=h, _patches=(rank // (world // 2),) if world > 1 else (0, 1))
         sh._configure(**kw)
         return sh
 

@@ -46,17 +46,27 @@ def test_plan_and_unique_id_handshake_gloo_world2():
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
-    assert got[0][0] == {"patches": (0,), "partner": 1}
-    assert got[1][0] == {"patches": (1,), "partner": 0}
+    assert got[0][0]["patches"] == (0,) and got[0][0]["partner"] == 1
+    assert got[1][0]["patches"] == (1,) and got[1][0]["partner"] == 0
     assert len(got[0][1]) == 128 and got[0][1] == got[1][1] and any(got[0][1])
 
 
-def test_plan_rejects_unbuilt_worlds():
+def test_plan_layout():
+    """Yin on the first nslab ranks, Yang on the rest; fringe partner = same slab of
+    the other patch, slab neighbours within the patch."""
     from paper_1905_02300_b200 import dist
-    assert dist.plan(1, 0) == {"patches": (0, 1), "partner": None}
-    for world in (3, 4, 8):
+    assert dist.plan(1, 0)["patches"] == (0, 1)
+    p = [dist.plan(8, r, nr=512) for r in range(8)]
+    assert [q["patch"] for q in p] == [0, 0, 0, 0, 1, 1, 1, 1]
+    assert [q["slab"] for q in p] == [0, 1, 2, 3, 0, 1, 2, 3]
+    assert [q["partner"] for q in p] == [4, 5, 6, 7, 0, 1, 2, 3]
+    assert [q["below"] for q in p] == [None, 0, 1, 2, None, 4, 5, 6]
+    assert [q["above"] for q in p] == [1, 2, 3, None, 5, 6, 7, None]
+    for world in (3, 6, 32):
         with pytest.raises(ValueError):
             dist.plan(world, 0)
+    with pytest.raises(ValueError):
+        dist.plan(8, 0, nr=96 + 2)       # 98 rows do not split into 4 slabs
 
 
 def _fields_all(shells, p, lev, s):
@@ -129,7 +139,7 @@ def _assemble(shells, p, lev, s):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nslab,case", [(2, "c1"), (2, "random"), (4, "convection")])
+@pytest.mark.parametrize("nslab,case", [(2, "c1"), (2, "random"), (4, "convection"), (2, "c3rows"), (4, "c3rows")])
 def test_radial_slabs_match_oracle(nslab, case):
     """Radial slabs (r-halos, partitioned r-sweep across slabs, per-slab norms)
     against the oracle: the slab solve changes only the rounding order of the
@@ -140,8 +150,10 @@ def test_radial_slabs_match_oracle(nslab, case):
     elif case == "random":
         cfg = W.small("C1", 32, 13, 37, Ra=30.0, dt=2e-3)
         wl = W.random_state(cfg, seed=11, amp=5.0)
-    else:
+    elif case == "convection":
         cfg, wl = W.small("C3", 64, 14, 40), None
+    else:                                   # C3's 96 radial rows: slabs of 48 / 24 rows
+        cfg, wl = W.small("C3", 96, 14, 40), None
     wl = wl if wl is not None else W.make_workload(cfg)
     args = (cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
     group = Shell.slabs(*args, nslab=nslab)
