@@ -44,12 +44,18 @@ class Oracle:
     """Both patches of one shell, stepped with plain numpy."""
 
     def __init__(self, nr, nth, nph, R1, R2, Pr, Ra, dt, chi=1.0, max_iters=100, fixed_iters=0,
-                 factor_order=None):
+                 factor_order=None, schwarz="additive"):
         self.g = Grid(nr, nth, nph, R1, R2)
         self.prm = Params(Pr, Ra, dt, chi)
         self.ex = Exchange(self.g)
         self.max_iters = max_iters
         self.fixed_iters = fixed_iters
+        if schwarz not in ("additive", "multiplicative"):
+            raise ValueError(schwarz)
+        # additive (RD26): both patches take the other's iterate k-1.  multiplicative
+        # (Algorithm 1 as printed, P:L487-513): Yin first with Yang's iterate k-1,
+        # then Yang with Yin's fresh iterate k (SURVEY NEXT-1).
+        self.schwarz = schwarz
         self.order = dict(FACTOR_ORDER) if factor_order is None else factor_order
         self.t = 0.0
         g = self.g
@@ -275,6 +281,14 @@ class Oracle:
         k = 0
         while k < kmax:
             k += 1
+            if self.schwarz == "multiplicative":
+                rho = 0.0
+                for p in range(2):
+                    self._fill_fringe(p, cur, wnew)
+                    rho = max(rho, self._iterate_patch(p, cur[p], stat[p], wdiff[p]))
+                if not self.fixed_iters and rho < tol:
+                    break
+                continue
             # O5 (a): fringe of all 9 quantities from the other patch's iterate k-1
             fr = []
             for p in range(2):
@@ -315,6 +329,35 @@ class Oracle:
             s["n"] = cur[p]
         self.t = t + tau
         return k, rho
+
+    def _fill_fringe(self, p, cur, wnew):
+        """O5 for patch p alone: its fringe of all 9 quantities from the other
+        patch's current iterate, and its u_r wall faces at t_{n+1} (multiplicative
+        Schwarz, Algorithm 1 steps 1/3/7 in patch order)."""
+        d = cur[1 - p]
+        for name in ("T", "p1", "p2"):
+            tgt = d[name].copy()
+            self.ex.fill_scalar("C", tgt, d[name])
+            self._set_fringe(p, cur, name, tgt)
+        for s in (1, 2):
+            tgt = d[f"ur{s}"].copy()
+            self.ex.fill_scalar("R", tgt, d[f"ur{s}"])
+            self._set_fringe(p, cur, f"ur{s}", tgt)
+            tt, tp = d[f"ut{s}"].copy(), d[f"up{s}"].copy()
+            self.ex.fill_vector(tt, tp, d[f"ut{s}"], d[f"up{s}"])
+            self._set_fringe(p, cur, f"ut{s}", tt)
+            self._set_fringe(p, cur, f"up{s}", tp)
+        for s in (1, 2):
+            cur[p][f"ur{s}"][0] = wnew[p]["ur"][0]
+            cur[p][f"ur{s}"][-1] = wnew[p]["ur"][1]
+
+    def _set_fringe(self, p, cur, name, v):
+        kind = QKIND[name.rstrip("12")]
+        mask = ~self.g.solved_mask(kind)
+        if kind == "R":
+            mask[0] = False
+            mask[-1] = False
+        cur[p][name][mask] = v[mask]
 
     def _solve(self, p, q, name, R, astar, cur):
         for axis in self.order[q]:

@@ -135,3 +135,32 @@ def test_schwarz_iteration_converges_and_counts_recorded():
     cfg = W.small("C1", 4, 12, 28, Ra=1.0, dt=1e-3)
     o, _ = _run(cfg, 2)
     assert all(1 < k < 30 and r < 1e-10 for k, r in o.stats)
+
+
+def test_multiplicative_and_additive_fixed_points_agree():
+    """SURVEY NEXT-1 / S:L482: the multiplicative Schwarz of Algorithm 1 as printed
+    (Yin with Yang's k-1, then Yang with Yin's fresh k) and the
+    additive variant (RD26) iterate to the same per-step fixed point, within
+    10 tol, from the same inputs; with one iteration per step they differ (the
+    multiplicative Yang sweep sees the new Yin fringe)."""
+    import workloads as W
+    cfg = W.small("C1", 6, 12, 30, dt=1e-3)
+    wl = W.make_workload(cfg)
+    tol = 1e-10
+    out = {}
+    for mode in ("additive", "multiplicative"):
+        o = Oracle(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, schwarz=mode)
+        o.load_workload(wl)
+        o.step(2, tol)
+        assert all(r < tol for _, r in o.stats)
+        out[mode] = [o.get_fields(p, 0, s) for p in range(2) for s in (1, 2)]
+    for a, b in zip(out["additive"], out["multiplicative"]):
+        for k in a:
+            assert np.max(np.abs(a[k] - b[k])) <= 10 * tol, k
+    one = {}
+    for mode in ("additive", "multiplicative"):
+        o = Oracle(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, schwarz=mode, fixed_iters=1)
+        o.load_workload(wl)
+        o.step(1, tol)
+        one[mode] = o.get_fields(1, 0, 2)      # Yang
+    assert max(np.max(np.abs(one["additive"][k] - one["multiplicative"][k])) for k in one["additive"]) > 1e-12
