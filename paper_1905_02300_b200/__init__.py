@@ -5,7 +5,7 @@ sm_100a by ``csrc/build.sh``).  Argument marshalling only: every step of the
 hot path runs in the CUDA kernels of ``csrc/``.  There is no CPU fallback —
 importing :mod:`paper_1905_02300_b200.yy` raises if the library is missing.
 """
-from .yy import (YY_CHI, YY_FIXED_ITERS, YY_MAX_ITERS, YYError, Shell, lib_path,  # noqa: F401
+from .yy import (YY_CHI, YY_FIXED_ITERS, YY_MAX_ITERS, YY_SCHWARZ, YYError, Shell, lib_path,  # noqa: F401
                  load_library, nccl_unique_id)
 
-__all__ = ["Shell", "YYError", "load_library", "lib_path", "nccl_unique_id", "YY_CHI", "YY_MAX_ITERS", "YY_FIXED_ITERS"]
+__all__ = ["Shell", "YYError", "load_library", "lib_path", "nccl_unique_id", "YY_CHI", "YY_MAX_ITERS", "YY_FIXED_ITERS", "YY_SCHWARZ"]

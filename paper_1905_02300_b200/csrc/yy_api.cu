@@ -53,6 +53,7 @@ struct yy_ctx {
   // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
   int patch0 = 0;
   int nslab = 1, slab = 0, roff = 0, nr_glob = 0;   // radial slab of the patch (nslab > 1)
+  int schwarz = 0;             // 0 additive (RD26), 1 multiplicative (Algorithm 1 as printed)
   int mode = 0;
   int world = 1, rank = 0;
   void* nccl = nullptr;        // ncclComm_t
@@ -494,6 +495,7 @@ yy_ctx* ctx_of(std::vector<yy_ctx*>& cs, int rank) {
 }
 
 yy_status run_xfers(std::vector<yy_ctx*>& cs, const std::vector<Xfer>& ops) {
+  if (cs.empty() || ops.empty()) return YY_OK;
   yy_ctx* ctx = cs[0];
   if (ctx->mode == 2) {                           // NCCL: this rank's sends and receives, one group call
     NcclApi& N = nccl_api();
@@ -520,6 +522,15 @@ yy_status run_xfers(std::vector<yy_ctx*>& cs, const std::vector<Xfer>& ops) {
 }
 
 bool distributed(const std::vector<yy_ctx*>& cs) { return !(cs.size() == 1 && cs[0]->mode == 0); }
+bool has_patch(const std::vector<yy_ctx*>& cs, int p) {
+  for (const yy_ctx* c : cs) if (c->patch0 == p) return true;
+  return false;
+}
+std::vector<yy_ctx*> of_patch(const std::vector<yy_ctx*>& cs, int p) {
+  std::vector<yy_ctx*> out;
+  for (yy_ctx* c : cs) if (c->patch0 == p) out.push_back(c);
+  return out;
+}
 int world_of(const yy_ctx* c) { return 2 * c->nslab; }
 
 // N1: r-halo rows of one iterate field with the slab neighbours of the same patch
@@ -534,7 +545,7 @@ yy_status exchange_halos(std::vector<yy_ctx*>& cs, int f) {
   const int halo_lo = (K == KR) ? 1 : 0, halo_hi = (K == KR) ? nl + 2 : nl + 1;
   std::vector<Xfer> ops;
   for (int p = 0; p < 2; ++p)
-    for (int sl = 1; sl < S; ++sl) {
+    for (int sl = 1; sl < S && (c0->mode == 2 || has_patch(cs, p)); ++sl) {
       const int up = p * S + sl, dn = up - 1;      // slab sl and the one below it
       ops.push_back({up, dn, [=](yy_ctx* c) -> const double* { return c->it[f] + own_lo * plane; },
                      [=](yy_ctx* c) { return c->it[f] + halo_hi * plane; }, plane});
@@ -604,7 +615,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
       }
       std::vector<Xfer> ops;                      // N2: boundary rows of every slab to its patch group
       for (int p = 0; p < 2; ++p)
-        for (int a1 = 0; a1 < S; ++a1)
+        for (int a1 = 0; a1 < S && (cs[0]->mode == 2 || has_patch(cs, p)); ++a1)
           for (int b1 = 0; b1 < S; ++b1)
             ops.push_back({p * S + a1, p * S + b1, [](yy_ctx* c) -> const double* { return c->IF; },
                            [=](yy_ctx* c) { return c->IFall + (long long)a1 * nlines * 6; }, 6LL * nlines});
@@ -717,6 +728,29 @@ yy_status iter_solve(std::vector<yy_ctx*>& cs) {
   return YY_OK;
 }
 
+// O5 for target patch p only (multiplicative Schwarz): the other patch's contexts
+// evaluate p's fringe from their current iterate, p's contexts write it
+yy_status exchange_fringe_to(std::vector<yy_ctx*>& cs, int p) {
+  const int S = cs[0]->nslab;
+  for (yy_ctx* ctx : cs) {
+    if (ctx->patch0 != 1 - p) continue;
+    ProfScope ps(ctx, "fringe_pack", 3);
+    launch_fringe_pack(ctx->g, interp_args(ctx), ctx->fr_send, ctx->st);
+  }
+  const long long n = cs[0]->fr_n;
+  std::vector<Xfer> ops;
+  for (int sl = 0; sl < S; ++sl)
+    ops.push_back({(1 - p) * S + sl, p * S + sl, [](yy_ctx* c) -> const double* { return c->fr_send; },
+                   [](yy_ctx* c) { return c->fr_recv; }, n});
+  TRY(run_xfers(cs, ops));
+  for (yy_ctx* ctx : cs) {
+    if (ctx->patch0 != p) continue;
+    ProfScope ps(ctx, "fringe_unpack", 3);
+    launch_fringe_unpack(ctx->g, interp_args(ctx), ctx->fr_recv, ctx->st);
+  }
+  return YY_OK;
+}
+
 // O5 (N3): fringe of every patch from the other patch's iterate k-1
 yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
   if (!distributed(cs)) {
@@ -790,8 +824,16 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   double rho = INFINITY;
   while (k < kmax) {
     ++k;
-    TRY(exchange_fringe(cs));                              // O5
-    TRY(iter_solve(cs));                                   // O6-O9, local norms
+    if (ctx->schwarz == 1) {                               // multiplicative: Yin, then Yang with Yin's k
+      for (int p = 0; p < 2; ++p) {
+        TRY(exchange_fringe_to(cs, p));                    // O5 for patch p
+        std::vector<yy_ctx*> cp = of_patch(cs, p);
+        if (!cp.empty()) TRY(iter_solve(cp));              // O6-O9 on patch p
+      }
+    } else {
+      TRY(exchange_fringe(cs));                            // O5
+      TRY(iter_solve(cs));                                 // O6-O9, local norms
+    }
     TRY(reduce_group(cs));                                 // O10
     for (yy_ctx* c : cs) {
       yy_ctx* ctx = c;
@@ -1164,6 +1206,14 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
     case YY_FIXED_ITERS:
       if (v < 0) return fail(ctx, YY_EINVAL, "fixed_iters must be >= 0");
       ctx->fixed_iters = (int)v;
+      return YY_OK;
+    case YY_SCHWARZ:
+      if (v != 0 && v != 1) return fail(ctx, YY_EINVAL, "schwarz must be 0 (additive) or 1 (multiplicative)");
+      if (v == 1 && ctx->g.npatch == 2)
+        return fail(ctx, YY_EINVAL, "multiplicative Schwarz needs one patch per context (yy_create_pair/_slabs/_dist)");
+      ctx->schwarz = (int)v;
+      if (ctx->mode == 1)
+        for (yy_ctx* c : ctx->group) if (c) c->schwarz = (int)v;
       return YY_OK;
     case YY_PROFILE:
       cudaStreamSynchronize(ctx->st);

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 YY_OK, YY_ENOCONV = 0, 4
-YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE = 1, 2, 3, 4
+YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ = 1, 2, 3, 4, 5
 TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
@@ -165,7 +165,7 @@ class Shell:
         sh._configure(**kw)
         return sh
 
-    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None):
+    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None, schwarz=None):
         if chi is not None:
             self.set_param(YY_CHI, chi)
         if max_iters is not None:
@@ -174,6 +174,8 @@ class Shell:
             self.set_param(YY_FIXED_ITERS, fixed_iters)
         if stream is not None:
             self.set_stream(stream)
+        if schwarz is not None:
+            self.set_param(YY_SCHWARZ, {"additive": 0, "multiplicative": 1}[schwarz])
 
     # shapes of include/yy.h
     def shape(self, name):

@@ -175,3 +175,48 @@ def test_radial_slabs_match_oracle(nslab, case):
                     assert not np.isnan(b[k]).any(), (p, s, k)      # every row owned by exactly one slab
                     den = vmax if k in ("ur", "ut", "up") else max(np.max(np.abs(c[k])), 1e-300)
                     assert np.max(np.abs(b[k] - c[k])) / den <= 1e-11, (p, s, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nslab,case", [(1, "c1"), (1, "random"), (2, "convection")])
+def test_multiplicative_schwarz_matches_oracle(nslab, case):
+    """Algorithm 1 as printed (Yin first with Yang's iterate k-1,
+    then Yang with Yin's fresh iterate k), on one-patch contexts (pair / slabs),
+    against the multiplicative oracle: parity bar and equal Schwarz counts."""
+    from paper_1905_02300_b200 import Shell
+    if case == "c1":
+        cfg, wl = W.small("C1", 16, 12, 30, dt=1e-3), None
+    elif case == "random":
+        cfg = W.small("C1", 16, 13, 37, Ra=30.0, dt=2e-3)
+        wl = W.random_state(cfg, seed=11, amp=5.0)
+    else:
+        cfg, wl = W.small("C3", 32, 14, 40), None
+    wl = wl if wl is not None else W.make_workload(cfg)
+    args = (cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    group = Shell.pair(*args, schwarz="multiplicative") if nslab == 1 else \
+        Shell.slabs(*args, nslab=nslab, schwarz="multiplicative")
+    for sh in group:
+        sh.load_workload(wl)
+    o = Oracle(*args, schwarz="multiplicative")
+    o.load_workload(wl)
+    for _ in range(2):
+        group[0].step(1, cfg.tol)
+        o.step(1, cfg.tol)
+        assert group[0].stats()[-1][0] == o.stats[-1][0], (group[0].stats(), o.stats)
+        for p in range(2):
+            for s in (1, 2):
+                b = _assemble(group, p, 0, s)
+                c = o.get_fields(p, 0, s)
+                vmax = max(np.max(np.abs(c[q])) for q in ("ur", "ut", "up"))
+                for k in c:
+                    den = vmax if k in ("ur", "ut", "up") else max(np.max(np.abs(c[k])), 1e-300)
+                    assert np.max(np.abs(b[k] - c[k])) / den <= 1e-11, (p, s, k)
+
+
+@pytest.mark.gpu
+def test_multiplicative_needs_one_patch_per_context():
+    from paper_1905_02300_b200 import YY_SCHWARZ, Shell, YYError
+    cfg = W.small("C1", 4, 12, 28)
+    sh = Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    with pytest.raises(YYError):
+        sh.set_param(YY_SCHWARZ, 1)
