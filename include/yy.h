@@ -63,10 +63,13 @@ enum {
   YY_MAX_ITERS = 2,    /* Schwarz K_max (RD25); default 100                                  */
   YY_FIXED_ITERS = 3,  /* >0: run exactly this many iterations per step, ignore tol          */
   YY_PROFILE = 4,      /* !=0: time every kernel class with CUDA events (resets the table)   */
-  YY_SCHWARZ = 5       /* 0: additive (RD26, default); 1: multiplicative, Algorithm 1 as printed
+  YY_SCHWARZ = 5,      /* 0: additive (RD26, default); 1: multiplicative, Algorithm 1 as printed
                           (Yin with Yang's iterate k-1, then Yang with Yin's k).
                           Needs one patch per context (yy_create_dist, or the test-only
                           yy_create_pair / yy_create_slabs); set on every rank            */
+  YY_HEAT_ONLY = 6     /* !=0: the heat Douglas scheme eq:HeatDouglas alone: only
+                          T is solved (u, p stay as set, normally 0 so a* = 0), the
+                          momentum and pressure kernels are skipped, rho_k is T's norm      */
 };
 
 typedef struct {

@@ -54,6 +54,7 @@ struct yy_ctx {
   int patch0 = 0;
   int nslab = 1, slab = 0, roff = 0, nr_glob = 0;   // radial slab of the patch (nslab > 1)
   int schwarz = 0;             // 0 additive (RD26), 1 multiplicative (Algorithm 1 as printed)
+  bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   int mode = 0;
   int world = 1, rank = 0;
   void* nccl = nullptr;        // ncclComm_t
@@ -660,7 +661,7 @@ yy_status step_begin(yy_ctx* ctx) {
     launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
   }
   // O3: static right-hand sides
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < (ctx->heat_only ? 1 : 4); ++q) {
     StaticArgs a = static_args(ctx, q, t + 0.5 * tau);
     ProfScope ps(ctx, kname(std::string("static_") + QNAME[q]), 1);
     launch_static(g, q, a, st);
@@ -695,7 +696,10 @@ InterpArgs interp_args(yy_ctx* ctx) {
 // context's per-(slot, patch) norm sums
 yy_status iter_solve(std::vector<yy_ctx*>& cs) {
   TRY(solve_quantity(cs, QT, 1, 0));                     // O6
-  for (int s = 1; s <= 2; ++s) {                         // O7 / O9
+  for (yy_ctx* ctx : cs)
+    if (ctx->heat_only)
+      for (int q = 1; q < NSLOT; ++q) ctx->nblk[q] = 0;  // no momentum / pressure slots
+  for (int s = 1; s <= 2 && !cs[0]->heat_only; ++s) {    // O7 / O9
     const int base = (s == 1) ? 1 : 5;
     TRY(solve_quantity(cs, QUR, s, base + 0));
     TRY(solve_quantity(cs, QUT, s, base + 1));
@@ -1214,6 +1218,11 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       ctx->schwarz = (int)v;
       if (ctx->mode == 1)
         for (yy_ctx* c : ctx->group) if (c) c->schwarz = (int)v;
+      return YY_OK;
+    case YY_HEAT_ONLY:
+      ctx->heat_only = v != 0;
+      if (ctx->mode == 1)
+        for (yy_ctx* c : ctx->group) if (c) c->heat_only = ctx->heat_only;
       return YY_OK;
     case YY_PROFILE:
       cudaStreamSynchronize(ctx->st);

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 YY_OK, YY_ENOCONV = 0, 4
-YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ = 1, 2, 3, 4, 5
+YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ, YY_HEAT_ONLY = 1, 2, 3, 4, 5, 6
 TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
@@ -99,7 +99,8 @@ class Shell:
     """One Yin-Yang shell context (include/yy.h `yy_ctx`)."""
 
     def __init__(self, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3,
-                 chi=None, max_iters=None, fixed_iters=None, stream=None, _handle=None, _patches=(0, 1)):
+                 chi=None, max_iters=None, fixed_iters=None, stream=None, heat_only=False, _handle=None,
+                 _patches=(0, 1)):
         self.L = load_library()
         self.nr, self.nt, self.np_ = nr, ntheta, nphi
         self.patches = tuple(_patches)        # patches this context holds
@@ -119,6 +120,8 @@ class Shell:
             self.set_param(YY_FIXED_ITERS, fixed_iters)
         if stream is not None:
             self.set_stream(stream)
+        if heat_only:
+            self.set_param(YY_HEAT_ONLY, 1)
 
     @classmethod
     def pair(cls, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3, **kw):
