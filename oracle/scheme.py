@@ -27,7 +27,7 @@ import math
 
 import numpy as np
 
-from . import ops
+from . import fluxfix, ops
 from .grid import Exchange, Grid
 from .ops import FACTOR_ORDER, QKIND, Params, to_kind
 from .tridiag import thomas
@@ -44,7 +44,7 @@ class Oracle:
     """Both patches of one shell, stepped with plain numpy."""
 
     def __init__(self, nr, nth, nph, R1, R2, Pr, Ra, dt, chi=1.0, max_iters=100, fixed_iters=0,
-                 factor_order=None, schwarz="additive"):
+                 factor_order=None, schwarz="additive", flux_fix_eps=None):
         self.g = Grid(nr, nth, nph, R1, R2)
         self.prm = Params(Pr, Ra, dt, chi)
         self.ex = Exchange(self.g)
@@ -56,6 +56,8 @@ class Oracle:
         # (Algorithm 1 as printed): Yin first with Yang's iterate k-1,
         # then Yang with Yin's fresh iterate k.
         self.schwarz = schwarz
+        # Algorithm 1 step 4 (optional in the paper): None = off
+        self.flux_fix_eps = flux_fix_eps
         self.order = dict(FACTOR_ORDER) if factor_order is None else factor_order
         self.t = 0.0
         g = self.g
@@ -285,6 +287,7 @@ class Oracle:
                 rho = 0.0
                 for p in range(2):
                     self._fill_fringe(p, cur, wnew)
+                    self._flux_fix(p, cur, tol)
                     rho = max(rho, self._iterate_patch(p, cur[p], stat[p], wdiff[p]))
                 if not self.fixed_iters and rho < tol:
                     break
@@ -318,6 +321,8 @@ class Oracle:
                 for s in (1, 2):
                     cur[p][f"ur{s}"][0] = wnew[p]["ur"][0]
                     cur[p][f"ur{s}"][-1] = wnew[p]["ur"][1]
+            for p in range(2):
+                self._flux_fix(p, cur, tol)
             rho = 0.0
             for p in range(2):
                 rho = max(rho, self._iterate_patch(p, cur[p], stat[p], wdiff[p]))
@@ -350,6 +355,13 @@ class Oracle:
         for s in (1, 2):
             cur[p][f"ur{s}"][0] = wnew[p]["ur"][0]
             cur[p][f"ur{s}"][-1] = wnew[p]["ur"][1]
+
+    def _flux_fix(self, p, cur, tol):
+        """Algorithm 1 step 4 on both systems' interpolated velocities of patch p."""
+        if self.flux_fix_eps is None:
+            return
+        for s in (1, 2):
+            fluxfix.flux_fix(self.g, cur[p][f"ur{s}"], cur[p][f"ut{s}"], cur[p][f"up{s}"], tol, self.flux_fix_eps)
 
     def _set_fringe(self, p, cur, name, v):
         kind = QKIND[name.rstrip("12")]
