@@ -67,9 +67,14 @@ enum {
                           (Yin with Yang's iterate k-1, then Yang with Yin's k).
                           Needs one patch per context (yy_create_dist, or the test-only
                           yy_create_pair / yy_create_slabs); set on every rank            */
-  YY_HEAT_ONLY = 6     /* !=0: the heat Douglas scheme eq:HeatDouglas alone: only
+  YY_HEAT_ONLY = 6,    /* !=0: the heat Douglas scheme eq:HeatDouglas alone: only
                           T is solved (u, p stay as set, normally 0 so a* = 0), the
                           momentum and pressure kernels are skipped, rho_k is T's norm      */
+  YY_FLUX_FIX = 7      /* eps > 0: Algorithm 1 step 4 every
+                          iteration after the fringe exchange — if |net boundary flux| >= tol
+                          the fringe normal velocities become the minimiser of J with penalty
+                          eps (1e-6); 0 = off (default, as in the paper's runs).
+                          Whole patches only (not with radial slabs)                        */
 };
 
 typedef struct {

@@ -55,6 +55,8 @@ struct yy_ctx {
   int nslab = 1, slab = 0, roff = 0, nr_glob = 0;   // radial slab of the patch (nslab > 1)
   int schwarz = 0;             // 0 additive (RD26), 1 multiplicative (Algorithm 1 as printed)
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
+  double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
+  double flux_a2 = 0.0, flux_area = 0.0;   // |a|^2 and |dOmega| of one patch (host geometry)
   int mode = 0;
   int world = 1, rank = 0;
   void* nccl = nullptr;        // ncclComm_t
@@ -802,6 +804,23 @@ yy_status reduce_group(std::vector<yy_ctx*>& cs) {
   return YY_OK;
 }
 
+// Algorithm 1 step 4 on every context of the group (after its fringe exchange)
+void flux_fix(std::vector<yy_ctx*>& cs, double tol) {
+  for (yy_ctx* ctx : cs) {
+    if (!(ctx->flux_eps > 0)) continue;
+    FluxArgs fa{};
+    fa.ur[0] = ctx->it[FUR1]; fa.ur[1] = ctx->it[FUR2];
+    fa.ut[0] = ctx->it[FUT1]; fa.ut[1] = ctx->it[FUT2];
+    fa.up[0] = ctx->it[FUP1]; fa.up[1] = ctx->it[FUP2];
+    fa.a2 = ctx->flux_a2;
+    fa.area = ctx->flux_area;
+    fa.eps = ctx->flux_eps;
+    fa.tol = tol;
+    ProfScope ps(ctx, "flux_fix", 1);
+    launch_flux_fix(ctx->g, fa, ctx->st);
+  }
+}
+
 // O11: rotate levels, advance t (per context)
 void step_end(yy_ctx* ctx) {
   for (int f = 0; f < NF; ++f) {
@@ -832,10 +851,12 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
       for (int p = 0; p < 2; ++p) {
         TRY(exchange_fringe_to(cs, p));                    // O5 for patch p
         std::vector<yy_ctx*> cp = of_patch(cs, p);
+        flux_fix(cp, tol);                                 // Alg. 1 step 4 (optional)
         if (!cp.empty()) TRY(iter_solve(cp));              // O6-O9 on patch p
       }
     } else {
       TRY(exchange_fringe(cs));                            // O5
+      flux_fix(cs, tol);                                   // Alg. 1 step 4 (optional)
       TRY(iter_solve(cs));                                 // O6-O9, local norms
     }
     TRY(reduce_group(cs));                                 // O10
@@ -933,6 +954,19 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   auto vec = [](int n, auto f) { std::vector<double> v(n); for (int q = 0; q < n; ++q) v[q] = f(q); return v; };
   const double dr2 = dr * dr, dt2 = dth * dth;
   put(&g.rc, rc); put(&g.rf, rf); put(&g.sc, sc); put(&g.sf, sf); put(&g.cc, cc); put(&g.cf, cf);
+  {   // Algorithm 1 step 4 constants of one patch (theta sides, phi sides, walls; reading RD-E5)
+    double a2 = 0.0, area = 0.0;
+    for (int i = 0; i < nr; ++i) {
+      for (int side = 0; side < 2; ++side) {
+        const double at = rc[i] * sf[side ? nt : 0] * dr * h.dph, ap = rc[i] * dr * dth;
+        a2 += h.np * at * at + nt * ap * ap;
+        area += h.np * at + nt * ap;
+      }
+    }
+    for (int j = 0; j < nt; ++j) area += (rf[0] * rf[0] + rf[nr] * rf[nr]) * sc[j] * dth * h.dph * h.np;
+    ctx->flux_a2 = a2;
+    ctx->flux_area = area;
+  }
   // r at centres
   put(&g.ir_c, vec(nr, [&](int i) { return 1.0 / rc[i]; }));
   put(&g.ir2_c, vec(nr, [&](int i) { return 1.0 / (rc[i] * rc[i]); }));
@@ -1218,6 +1252,13 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       ctx->schwarz = (int)v;
       if (ctx->mode == 1)
         for (yy_ctx* c : ctx->group) if (c) c->schwarz = (int)v;
+      return YY_OK;
+    case YY_FLUX_FIX:
+      if (v < 0) return fail(ctx, YY_EINVAL, "flux-fix eps must be >= 0 (0 = off)");
+      if (v > 0 && ctx->nslab > 1) return fail(ctx, YY_EINVAL, "flux fix needs whole patches (no radial slabs)");
+      ctx->flux_eps = v;
+      if (ctx->mode == 1)
+        for (yy_ctx* c : ctx->group) if (c) c->flux_eps = v;
       return YY_OK;
     case YY_HEAT_ONLY:
       ctx->heat_only = v != 0;

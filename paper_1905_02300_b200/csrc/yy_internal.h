@@ -77,6 +77,14 @@ struct PresArgs {
   int maxb;
 };
 
+// Algorithm 1 step 4 (mass-flux correction)
+struct FluxArgs {
+  double *ur[2], *ut[2], *up[2];   // iterates of systems 1, 2 (all local patches)
+  double a2;                       // |a|^2: sum of the squared side-face areas (one patch)
+  double area;                     // |dOmega|: total closed-surface area (one patch)
+  double eps, tol;
+};
+
 struct ReduceArgs {
   int nblk[NSLOT];
   int maxb;
@@ -144,6 +152,7 @@ void launch_fringe_pack(const Geo& g, const InterpArgs& a, double* buf, cudaStre
 void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, cudaStream_t st);
 // out[2 + 2 slot + p] <- sum over slabs s (fixed order) of gath[p * nslab + s][2 + 2 slot + p]
 // (gath: every context's sums, world = 2 nslab contexts ordered rank = patch nslab + slab)
+void launch_flux_fix(const Geo& g, const FluxArgs& a, cudaStream_t st);
 void launch_merge_all(double* out, const double* gath, int nslab, cudaStream_t st);
 // slab r-sweeps: solve the 2 nslab boundary system of every line, then x = x0 + xlo X_LO + xhi X_HI
 void launch_slab_solve(const SlabArgs& a, cudaStream_t st);

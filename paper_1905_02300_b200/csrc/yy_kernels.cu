@@ -328,6 +328,67 @@ __global__ void k_unpack_vec(Geo g, InterpArgs a, const double* __restrict__ buf
 }
 
 // ---------------------------------------------------------------------------------
+// Algorithm 1 step 4: if |oint u_bd . n| >= tol over the
+// patch's cell-box surface (the fringe normal velocities u_theta(j = 0, nt),
+// u_phi(k = 0, np) and the walls u_r(i = 0, nr); reading RD-E5), replace the side
+// values by the minimiser of J:  v = u - mu a, mu = (a.u + b) / (eps |dOmega|^2 + |a|^2)
+// (a = signed side-face areas, b = wall flux; the paper reaches it by CG, J is
+// quadratic with a rank-one penalty).  One block per (local patch, system); the
+// flux is a fixed-order sum (deterministic).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_flux_fix(Geo g, FluxArgs a) {
+  const int p = blockIdx.x / 2, s = blockIdx.x % 2;
+  double* ur = a.ur[s] + p * psize(g, KR);
+  double* ut = a.ut[s] + p * psize(g, KT);
+  double* up = a.up[s] + p * psize(g, KP);
+  const int nr = g.nr, nt = g.nt, np = g.np;
+  const double s0 = __ldg(g.sf), s1 = __ldg(g.sf + nt);
+  double f = 0.0;
+  // theta sides: (side, i, k), area -/+ r_c sin(theta_f) dr dphi
+  for (int q = threadIdx.x; q < 2 * nr * np; q += blockDim.x) {
+    const int side = q / (nr * np), i = (q / np) % nr, k = q % np;
+    const double ar = __ldg(g.rc + i) * (side ? s1 : -s0) * g.dr * g.dph;
+    f += ar * ut[IX<KT>(g, i, side ? nt : 0, k)];
+  }
+  // phi sides: (side, i, j), area -/+ r_c dr dtheta
+  for (int q = threadIdx.x; q < 2 * nr * nt; q += blockDim.x) {
+    const int side = q / (nr * nt), i = (q / nt) % nr, j = q % nt;
+    const double ar = __ldg(g.rc + i) * (side ? 1.0 : -1.0) * g.dr * g.dth;
+    f += ar * up[IX<KP>(g, i, j, side ? np : 0)];
+  }
+  // walls: (wall, j, k), area -/+ r_f^2 sin(theta_c) dtheta dphi
+  for (int q = threadIdx.x; q < 2 * nt * np; q += blockDim.x) {
+    const int w = q / (nt * np), j = (q / np) % nt, k = q % np;
+    const double rf = __ldg(g.rf + (w ? nr : 0));
+    const double ar = (w ? 1.0 : -1.0) * rf * rf * __ldg(g.sc + j) * g.dth * g.dph;
+    f += ar * ur[IX<KR>(g, w ? nr : 0, j, k)];
+  }
+  __shared__ double sh[16];
+  __shared__ double s_mu;
+  for (int o = 16; o > 0; o >>= 1) f += __shfl_down_sync(0xffffffffu, f, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double F = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) F += sh[w];
+    s_mu = (fabs(F) >= a.tol) ? F / (a.eps * a.area * a.area + a.a2) : 0.0;
+  }
+  __syncthreads();
+  const double mu = s_mu;
+  if (mu == 0.0) return;
+  for (int q = threadIdx.x; q < 2 * nr * np; q += blockDim.x) {
+    const int side = q / (nr * np), i = (q / np) % nr, k = q % np;
+    const double ar = __ldg(g.rc + i) * (side ? s1 : -s0) * g.dr * g.dph;
+    ut[IX<KT>(g, i, side ? nt : 0, k)] -= mu * ar;
+  }
+  for (int q = threadIdx.x; q < 2 * nr * nt; q += blockDim.x) {
+    const int side = q / (nr * nt), i = (q / nt) % nr, j = q % nt;
+    const double ar = __ldg(g.rc + i) * (side ? 1.0 : -1.0) * g.dr * g.dth;
+    up[IX<KP>(g, i, j, side ? np : 0)] -= mu * ar;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------------
 static inline dim3 pgrid(const Geo& g, int K, int npatch) {
@@ -419,5 +480,9 @@ void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, 
   if (a.tab_ph.n) k_unpack_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bph);
 }
 
+
+void launch_flux_fix(const Geo& g, const FluxArgs& a, cudaStream_t st) {
+  k_flux_fix<<<2 * g.npatch, 512, 0, st>>>(g, a);
+}
 
 }  // namespace yy

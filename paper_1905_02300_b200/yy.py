@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 YY_OK, YY_ENOCONV = 0, 4
-YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ, YY_HEAT_ONLY = 1, 2, 3, 4, 5, 6
+YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ, YY_HEAT_ONLY, YY_FLUX_FIX = 1, 2, 3, 4, 5, 6, 7
 TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
@@ -99,8 +99,8 @@ class Shell:
     """One Yin-Yang shell context (include/yy.h `yy_ctx`)."""
 
     def __init__(self, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3,
-                 chi=None, max_iters=None, fixed_iters=None, stream=None, heat_only=False, _handle=None,
-                 _patches=(0, 1)):
+                 chi=None, max_iters=None, fixed_iters=None, stream=None, heat_only=False, flux_fix_eps=None,
+                 _handle=None, _patches=(0, 1)):
         self.L = load_library()
         self.nr, self.nt, self.np_ = nr, ntheta, nphi
         self.patches = tuple(_patches)        # patches this context holds
@@ -122,6 +122,8 @@ class Shell:
             self.set_stream(stream)
         if heat_only:
             self.set_param(YY_HEAT_ONLY, 1)
+        if flux_fix_eps is not None:
+            self.set_param(YY_FLUX_FIX, flux_fix_eps)
 
     @classmethod
     def pair(cls, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3, **kw):
@@ -168,7 +170,7 @@ class Shell:
         sh._configure(**kw)
         return sh
 
-    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None, schwarz=None):
+    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None, schwarz=None, flux_fix_eps=None):
         if chi is not None:
             self.set_param(YY_CHI, chi)
         if max_iters is not None:
@@ -179,6 +181,8 @@ class Shell:
             self.set_stream(stream)
         if schwarz is not None:
             self.set_param(YY_SCHWARZ, {"additive": 0, "multiplicative": 1}[schwarz])
+        if flux_fix_eps is not None:
+            self.set_param(YY_FLUX_FIX, flux_fix_eps)
 
     # shapes of include/yy.h
     def shape(self, name):

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
 """Additive (RD26) vs multiplicative (Algorithm 1 as printed)
+Schwarz, and the mass-flux correction on/off,
 Schwarz on C3 with one patch per context (yy_create_pair on one GPU): device
 time per step and Schwarz iterations per step."""
 import json
@@ -27,6 +28,14 @@ def main():
         out[mode] = {"ms_per_step": ms, "schwarz_iters": ks, "cell_updates_per_s": 2 * cfg.cells / (ms / 1e3)}
         for sh in g:
             sh.close()
+    # Algorithm 1 step 4 on the single context
+    for eps in (None, 1e-6):
+        sh = Shell(*args, flux_fix_eps=eps)
+        sh.load_workload(wl)
+        ms, ks = time_step([sh], cfg, steps=3)
+        out["single" + ("+flux_fix" if eps else "")] = {"ms_per_step": ms, "schwarz_iters": ks,
+                                                       "cell_updates_per_s": 2 * cfg.cells / (ms / 1e3)}
+        sh.close()
     print(json.dumps({"workload": "C3", "layout": "yy_create_pair (one patch per context, one GPU)", "modes": out}))
 
 
