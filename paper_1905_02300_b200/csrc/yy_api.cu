@@ -56,6 +56,7 @@ struct yy_ctx {
   int schwarz = 0;             // 0 additive (RD26), 1 multiplicative (Algorithm 1 as printed)
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
+  double* bsplit[4][3] = {};   // split-row tables (Geo::bsplit)
   double flux_a2 = 0.0, flux_area = 0.0;   // |a|^2 and |dOmega| of one patch (host geometry)
   int mode = 0;
   int world = 1, rank = 0;
@@ -1061,6 +1062,12 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
         (s = dalloc(ctx, &ctx->LH, 2 * nlmax)) != YY_OK) { yy_destroy(ctx); return s; }
   }
   ctx->rank = patch0 * nslab + slab;
+  for (int q = 0; q < 4; ++q)
+    for (int ax = 0; ax < 3; ++ax) {
+      if ((s = dalloc(ctx, &ctx->bsplit[q][ax], (size_t)3 * NRk(g, q) * NTk(g, q))) != YY_OK) { yy_destroy(ctx); return s; }
+      g.bsplit[q][ax] = ctx->bsplit[q][ax];
+    }
+  launch_build_split(g, ctx->bsplit, ctx->st);
   if (cudaDeviceSynchronize() != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
   *out = ctx;
   return YY_OK;
@@ -1236,6 +1243,8 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       ctx->chi = v;
       ctx->g.cchi = 1.0 / (2.0 * v);
       ctx->g.inv_chi = 1.0 / v;
+      launch_build_split(ctx->g, ctx->bsplit, ctx->st);   // the D_ii rows carry c_chi
+      CK(cudaStreamSynchronize(ctx->st));
       return YY_OK;
     case YY_MAX_ITERS:
       if (v < 1) return fail(ctx, YY_EINVAL, "max_iters must be >= 1");

@@ -46,6 +46,10 @@ struct Geo {
   const double *ir_f, *ir2_f, *lr_fm, *lr_fp, *mr_m, *mr_p, *d11_m, *d11_p, *d11_0, *rf2;   // [nr+1]
   const double *is_c, *is2_c, *cot_c, *lt_cm, *lt_cp;                    // [nt]
   const double *is_f, *is2_f, *cot_f, *lt_fm, *lt_fp, *mt_m, *mt_p, *d22_m, *d22_p, *d22_0;  // [nt+1]
+  // a*-independent part of the split (hat) rows of every (quantity, axis):
+  // [i][j][am, a0, ap] over the kind's (r, theta) nodes (k-independent), built once
+  // on the device from coef<Q, AX, true, false> (yy_kernels.cu: k_build_split)
+  const double* bsplit[4][3];
 };
 
 // 1/x to full fp64 precision (<= 1 ulp): hardware approximation refined by two
@@ -149,7 +153,8 @@ template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {  
 // HAT selects the implicit (split) operator with Delta^_thth, Delta^_phph
 // versus the full Delta_thth, Delta_phph of the explicit L psi^*.
 // Weights are products of the 1-D tables of Geo (see yy_api.cu: host_tables).
-template <int Q, int AX, bool HAT>
+// ADV = false: the transport-velocity terms left out (a* = 0), for the tables.
+template <int Q, int AX, bool HAT, bool ADV = true>
 __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j, int k,
                                      double& am, double& a0, double& ap) {
   constexpr int K = kind_of(Q);
@@ -158,7 +163,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     // Delta_rr = (1/r^2) d_r(r^2 d_r), flux form; - a_r d_r
     const double dm = D * (K == KR ? __ldg(g.lr_fm + i) : __ldg(g.lr_cm + i));
     const double dp = D * (K == KR ? __ldg(g.lr_fp + i) : __ldg(g.lr_cp + i));
-    const double adv = abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
+    const double adv = ADV ? abar_r<K>(g, A, i, j, k) * (0.5 * g.idr) : 0.0;
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
@@ -176,7 +181,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     const double rho = HAT ? g.iR1sq : ir2n<K>(g, i);
     const double dm = D * rho * (K == KT ? __ldg(g.lt_fm + j) : __ldg(g.lt_cm + j));
     const double dp = D * rho * (K == KT ? __ldg(g.lt_fp + j) : __ldg(g.lt_cp + j));
-    const double adv = abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
+    const double adv = ADV ? abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i) : 0.0;
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
@@ -190,13 +195,13 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
       ap += g.cchi * ir2 * __ldg(g.d22_p + j);
       am += g.cchi * ir2 * __ldg(g.d22_m + j);
       a0 -= g.cchi * ir2 * __ldg(g.d22_0 + j);
-      a0 -= abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
+      if (ADV) a0 -= abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
     }
   } else {
     // Delta_phph = d_phph/(r^2 sin^2 th); hat: 1/(R1^2 sin^2 th_1); - (a_ph/(r sin th)) d_ph
     const double ir = irn<K>(g, i), is = isn<K>(g, j);
     const double c = HAT ? D * g.hatph : D * ir2n<K>(g, i) * is2n<K>(g, j) * g.idph2;
-    const double adv = abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is;
+    const double adv = ADV ? abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is : 0.0;
     am = c + adv;
     ap = c - adv;
     a0 = -2.0 * c;
@@ -208,9 +213,43 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
       am += c2;
       ap += c2;
       a0 -= 2.0 * c2;
-      a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
+      if (ADV) a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
     }
   }
+}
+
+// The split (hat) rows of L_{Q,AX} at node (i,j,k) = the tabulated a*-independent
+// part (Geo::bsplit) + the transport-velocity terms: the same rows as
+// coef<Q,AX,true> up to the order of the additions, with 3 table loads instead of
+// the 1-D factor products.
+template <int Q, int AX>
+__device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, int j, int k,
+                                           double& am, double& a0, double& ap) {
+  constexpr int K = kind_of(Q);
+  // tabulated only where the own-direction row carries the metric / grad-div
+  // terms (u_r in r, u_th in theta, u_ph in phi); measured on B200 (C3), the
+  // plain Laplacian rows are cheaper from the 1-D factors
+  if constexpr (!((Q == QUR && AX == 0) || (Q == QUT && AX == 1) || (Q == QUP && AX == 2))) {
+    coef<Q, AX, true>(g, A, i, j, k, am, a0, ap);
+    return;
+  }
+  const double* b = g.bsplit[Q][AX] + 3 * (i * NTk(g, K) + j);
+  am = __ldg(b);
+  a0 = __ldg(b + 1);
+  ap = __ldg(b + 2);
+  double adv;
+  if (AX == 0) {
+    adv = abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
+  } else if (AX == 1) {
+    adv = abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
+    if (Q == QUT) a0 -= abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
+  } else {
+    adv = abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * irn<K>(g, i) * isn<K>(g, j);
+    if (Q == QUP)
+      a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
+  }
+  am += adv;
+  ap -= adv;
 }
 
 // Solved-node ranges of a kind (reading RD3): fringe = outermost theta/phi

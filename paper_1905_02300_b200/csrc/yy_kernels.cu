@@ -389,6 +389,24 @@ __global__ void __launch_bounds__(512) k_flux_fix(Geo g, FluxArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
+// Setup: the a*-independent split rows of (Q, AX) at every (i, j) of Q's kind,
+// from the same coef<> the full rows use (Geo::bsplit; rebuilt when chi changes)
+// ---------------------------------------------------------------------------------
+template <int Q, int AX>
+__global__ void k_build_split(Geo g, double* __restrict__ out) {
+  constexpr int K = kind_of(Q);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= NRk(g, K) * NTk(g, K)) return;
+  const int i = q / NTk(g, K), j = q % NTk(g, K);
+  const Astar none{nullptr, nullptr, nullptr};
+  double am, a0, ap;
+  coef<Q, AX, true, false>(g, none, i, j, 1, am, a0, ap);
+  out[3 * q] = am;
+  out[3 * q + 1] = a0;
+  out[3 * q + 2] = ap;
+}
+
+// ---------------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------------
 static inline dim3 pgrid(const Geo& g, int K, int npatch) {
@@ -483,6 +501,22 @@ void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, 
 
 void launch_flux_fix(const Geo& g, const FluxArgs& a, cudaStream_t st) {
   k_flux_fix<<<2 * g.npatch, 512, 0, st>>>(g, a);
+}
+
+template <int Q>
+static void build_split_q(const Geo& g, double* const (&dst)[3], cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  const int n = NRk(g, K) * NTk(g, K), b = (n + 127) / 128;
+  k_build_split<Q, 0><<<b, 128, 0, st>>>(g, dst[0]);
+  k_build_split<Q, 1><<<b, 128, 0, st>>>(g, dst[1]);
+  k_build_split<Q, 2><<<b, 128, 0, st>>>(g, dst[2]);
+}
+
+void launch_build_split(const Geo& g, double* const (&dst)[4][3], cudaStream_t st) {
+  build_split_q<QT>(g, dst[0], st);
+  build_split_q<QUR>(g, dst[1], st);
+  build_split_q<QUT>(g, dst[2], st);
+  build_split_q<QUP>(g, dst[3], st);
 }
 
 }  // namespace yy

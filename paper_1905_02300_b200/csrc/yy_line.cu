@@ -241,7 +241,7 @@ __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, in
   constexpr int K = kind_of(Q);
   const double th = 0.5 * g.tau;
   double am, a0, ap;
-  coef<Q, AX, true>(g, A, i, j, k, am, a0, ap);
+  coef_split<Q, AX>(g, A, i, j, k, am, a0, ap);
   double di = 1.0 - th * a0;
   if (AX == 0 && K != KR) {          // antisymmetric wall ghost of the increment (RD23)
     if (m == 0 && g.wall_lo) di = 1.0 - th * (a0 - am);

@@ -56,11 +56,14 @@ __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict
 template <int Q, bool HAT>
 __device__ __forceinline__ double applyL(const Geo& g, const Astar& A, int i, int j, int k, const Star& s) {
   double am, a0, ap, acc;
-  coef<Q, 0, HAT>(g, A, i, j, k, am, a0, ap);
+  if (HAT) coef_split<Q, 0>(g, A, i, j, k, am, a0, ap);
+  else coef<Q, 0, false>(g, A, i, j, k, am, a0, ap);
   acc = am * s.xm + a0 * s.c + ap * s.xp;
-  coef<Q, 1, HAT>(g, A, i, j, k, am, a0, ap);
+  if (HAT) coef_split<Q, 1>(g, A, i, j, k, am, a0, ap);
+  else coef<Q, 1, false>(g, A, i, j, k, am, a0, ap);
   acc += am * s.ym + a0 * s.c + ap * s.yp;
-  coef<Q, 2, HAT>(g, A, i, j, k, am, a0, ap);
+  if (HAT) coef_split<Q, 2>(g, A, i, j, k, am, a0, ap);
+  else coef<Q, 2, false>(g, A, i, j, k, am, a0, ap);
   acc += am * s.zm + a0 * s.c + ap * s.zp;
   return acc;
 }
