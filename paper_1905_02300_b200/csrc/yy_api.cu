@@ -57,6 +57,8 @@ struct yy_ctx {
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
   double* bsplit[4][3] = {};   // split-row tables (Geo::bsplit)
+  double* react_t = nullptr;   // Astar::rt, Astar::rp (per step)
+  double* react_p = nullptr;
   double flux_a2 = 0.0, flux_area = 0.0;   // |a|^2 and |dOmega| of one patch (host geometry)
   int mode = 0;
   int world = 1, rank = 0;
@@ -407,6 +409,7 @@ yy_status eval_walls(yy_ctx* ctx, int L, double t) {
 StaticArgs static_args(yy_ctx* ctx, int q, double tsrc) {
   StaticArgs a{};
   a.ar = ctx->astar[0]; a.at = ctx->astar[1]; a.ap = ctx->astar[2];
+  a.rt = ctx->react_t; a.rp = ctx->react_p;
   const int f1 = (q == QT) ? FT : (q == QUR ? FUR1 : q == QUT ? FUT1 : FUP1);
   const int f2 = (q == QT) ? FT : f1 + 3;
   a.fn[0] = ctx->n[f1]; a.fn[1] = ctx->n[f2];
@@ -571,6 +574,7 @@ ResidArgs resid_args(yy_ctx* ctx, int q, int s) {
   r.wnew = wf >= 0 ? ctx->wl[2][wf] : nullptr;
   r.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
   r.ar = ctx->astar[0]; r.at = ctx->astar[1]; r.ap = ctx->astar[2];
+  r.rt = ctx->react_t; r.rp = ctx->react_p;
   r.G = ctx->G[f];
   r.R = ctx->R;
   r.Tit = ctx->it[FT]; r.Tn = ctx->n[FT];
@@ -584,6 +588,7 @@ ResidArgs resid_args(yy_ctx* ctx, int q, int s) {
 SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
   SweepArgs w{};
   w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
+  w.rt = ctx->react_t; w.rp = ctx->react_p;
   w.R = ctx->R; w.psi = ctx->it[qfield(q, s)];
   w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
   w.maxb = ctx->maxb;
@@ -662,6 +667,10 @@ yy_status step_begin(yy_ctx* ctx) {
     in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
     ProfScope ps(ctx, "astar", 1);
     launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
+  }
+  {
+    ProfScope ps(ctx, "react", 1);
+    launch_react(g, ctx->astar[0], ctx->astar[1], ctx->react_t, ctx->react_p, st);
   }
   // O3: static right-hand sides
   for (int q = 0; q < (ctx->heat_only ? 1 : 4); ++q) {
@@ -1030,6 +1039,10 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   }
   for (int c = 0; c < 3; ++c)
     if ((s = dalloc(ctx, &ctx->astar[c], npatch * psize(g, KR + c))) != YY_OK) { yy_destroy(ctx); return s; }
+  if ((s = dalloc(ctx, &ctx->react_t, npatch * psize(g, KT))) != YY_OK ||
+      (s = dalloc(ctx, &ctx->react_p, npatch * psize(g, KP))) != YY_OK) { yy_destroy(ctx); return s; }
+  cudaMemset(ctx->react_t, 0, npatch * psize(g, KT) * sizeof(double));
+  cudaMemset(ctx->react_p, 0, npatch * psize(g, KP) * sizeof(double));
   if ((s = dalloc(ctx, &ctx->R, npatch * maxk)) != YY_OK) { yy_destroy(ctx); return s; }
   cudaMemset(ctx->R, 0, npatch * maxk * sizeof(double));
   // norm partials: max blocks per (slot, patch)

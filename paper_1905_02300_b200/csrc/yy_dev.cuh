@@ -93,6 +93,11 @@ struct Astar {
   const double* __restrict__ ar;   // kind R
   const double* __restrict__ at;   // kind TH
   const double* __restrict__ ap;   // kind PH
+  // the a*-reaction coefficients of the own-direction rows, evaluated once per step
+  // (k_react): rt = abar_r<TH> / r at u_theta nodes (RD14), rp = (abar_r<PH> +
+  // abar_t<PH> cot(theta)) / r at u_phi nodes
+  const double* __restrict__ rt;
+  const double* __restrict__ rp;
 };
 
 // a*_r averaged to the nodes of kind K (average along every axis where the
@@ -154,7 +159,10 @@ template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {  
 // versus the full Delta_thth, Delta_phph of the explicit L psi^*.
 // Weights are products of the 1-D tables of Geo (see yy_api.cu: host_tables).
 // ADV = false: the transport-velocity terms left out (a* = 0), for the tables.
-template <int Q, int AX, bool HAT, bool ADV = true>
+// RX: the reaction terms from the per-step arrays Astar::rt/rp (the sweeps) instead
+// of from the a* averages (the residual and static kernels, which load those a*
+// values for the other terms anyway).
+template <int Q, int AX, bool HAT, bool ADV = true, bool RX = false>
 __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j, int k,
                                      double& am, double& a0, double& ap) {
   constexpr int K = kind_of(Q);
@@ -195,7 +203,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
       ap += g.cchi * ir2 * __ldg(g.d22_p + j);
       am += g.cchi * ir2 * __ldg(g.d22_m + j);
       a0 -= g.cchi * ir2 * __ldg(g.d22_0 + j);
-      if (ADV) a0 -= abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
+      if (ADV) a0 -= RX ? __ldg(A.rt + IX<KT>(g, i, j, k)) : abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
     }
   } else {
     // Delta_phph = d_phph/(r^2 sin^2 th); hat: 1/(R1^2 sin^2 th_1); - (a_ph/(r sin th)) d_ph
@@ -213,7 +221,9 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
       am += c2;
       ap += c2;
       a0 -= 2.0 * c2;
-      if (ADV) a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
+      if (ADV)
+        a0 -= RX ? __ldg(A.rp + IX<KP>(g, i, j, k))
+                 : (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
     }
   }
 }
@@ -222,7 +232,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
 // part (Geo::bsplit) + the transport-velocity terms: the same rows as
 // coef<Q,AX,true> up to the order of the additions, with 3 table loads instead of
 // the 1-D factor products.
-template <int Q, int AX>
+template <int Q, int AX, bool RX = false>
 __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, int j, int k,
                                            double& am, double& a0, double& ap) {
   constexpr int K = kind_of(Q);
@@ -230,7 +240,7 @@ __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, 
   // terms (u_r in r, u_th in theta, u_ph in phi); measured on B200 (C3), the
   // plain Laplacian rows are cheaper from the 1-D factors
   if constexpr (!((Q == QUR && AX == 0) || (Q == QUT && AX == 1) || (Q == QUP && AX == 2))) {
-    coef<Q, AX, true>(g, A, i, j, k, am, a0, ap);
+    coef<Q, AX, true, true, RX>(g, A, i, j, k, am, a0, ap);
     return;
   }
   const double* b = g.bsplit[Q][AX] + 3 * (i * NTk(g, K) + j);
@@ -242,11 +252,12 @@ __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, 
     adv = abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
   } else if (AX == 1) {
     adv = abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
-    if (Q == QUT) a0 -= abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
+    if (Q == QUT) a0 -= RX ? __ldg(A.rt + IX<KT>(g, i, j, k)) : abar_r<K>(g, A, i, j, k) * __ldg(g.ir_c + i);
   } else {
     adv = abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * irn<K>(g, i) * isn<K>(g, j);
     if (Q == QUP)
-      a0 -= (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
+      a0 -= RX ? __ldg(A.rp + IX<KP>(g, i, j, k))
+               : (abar_r<K>(g, A, i, j, k) + abar_t<K>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
   }
   am += adv;
   ap -= adv;

@@ -21,6 +21,7 @@ struct StaticArgs {
   const double* wn;          // wall data at t_n (2 patches x 2 walls x plane), NULL for u_r
   const double* wm;          // wall data at t_{n-1}
   const double *ar, *at, *ap;  // a*
+  const double *rt, *rp;     // a*-reaction coefficients (Astar)
   const double* p[2];        // p1^n, p2^n
   const double* utn[2];      // u_th^n, u_th^{n-1} per system (for u_th^*)
   const double* utm[2];
@@ -38,6 +39,7 @@ struct ResidArgs {
   const double* wnew;        // wall data t_{n+1}
   const double* wn;          // wall data t_n
   const double *ar, *at, *ap;
+  const double *rt, *rp;
   const double* G;
   double* R;
   const double *Tit, *Tn;    // for u_r buoyancy
@@ -48,6 +50,7 @@ struct ResidArgs {
 
 struct SweepArgs {
   const double *ar, *at, *ap;
+  const double *rt, *rp;
   double* R;                 // in: rhs, out: solution (non-final); slab r-sweep: x0
   double* C;                 // unused
   double* psi;               // FINAL: psi += x
@@ -115,6 +118,8 @@ struct InterpArgs {
 };
 
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);
+// per step, after a*: the reaction coefficients rt (TH nodes), rp (PH nodes) of Astar
+void launch_react(const Geo& g, const double* ar, const double* at, double* rt, double* rp, cudaStream_t st);
 void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st);
 void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t st);
 inline int max_line_len(int ax) { return ax == 2 ? 32 * 36 : 32 * 16; }   // unknowns per line (yy_line.cu)

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
   const long long po = patch * psize(g, K);
   const long long pc = patch * psize(g, KC);
   const int node = IX<K>(g, i, j, k);
-  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
+          a.rt + patch * psize(g, KT), a.rp + patch * psize(g, KP)};
   const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
   const double* Wm = a.wm ? a.wm + patch * 2 * wsize(g, K) : nullptr;
   double src = 0.0;
@@ -398,12 +399,32 @@ __global__ void k_build_split(Geo g, double* __restrict__ out) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= NRk(g, K) * NTk(g, K)) return;
   const int i = q / NTk(g, K), j = q % NTk(g, K);
-  const Astar none{nullptr, nullptr, nullptr};
+  const Astar none{nullptr, nullptr, nullptr, nullptr, nullptr};
   double am, a0, ap;
   coef<Q, AX, true, false>(g, none, i, j, 1, am, a0, ap);
   out[3 * q] = am;
   out[3 * q + 1] = a0;
   out[3 * q + 2] = ap;
+}
+
+// ---------------------------------------------------------------------------------
+// per step (a* is fixed for the step, RD8): the a*-reaction coefficients of the
+// u_theta theta-rows (RD14) and u_phi phi-rows, read by every
+// residual, static RHS and own-direction sweep of both systems instead of their
+// 4-point a* averages.  grid: x -> k, y -> j, z -> patch * nr + i
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_react(Geo g, const double* __restrict__ ar, const double* __restrict__ at,
+                                               double* __restrict__ rt, double* __restrict__ rp) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int patch = blockIdx.z / g.nr, i = blockIdx.z % g.nr;
+  const Astar A{ar + patch * psize(g, KR), at + patch * psize(g, KT), nullptr, nullptr, nullptr};
+  // u_theta nodes (i, j in 1..nt-1, k) and u_phi nodes (i, j, k in 1..np-1): interior of the averages
+  if (j >= 1 && j <= NTk(g, KT) - 2 && k >= 1 && k <= NPk(g, KT) - 2 && i >= 0 && i < g.nr)
+    rt[patch * psize(g, KT) + IX<KT>(g, i, j, k)] = abar_r<KT>(g, A, i, j, k) * __ldg(g.ir_c + i);
+  if (j >= 1 && j <= NTk(g, KP) - 2 && k >= 1 && k <= NPk(g, KP) - 2)
+    rp[patch * psize(g, KP) + IX<KP>(g, i, j, k)] =
+        (abar_r<KP>(g, A, i, j, k) + abar_t<KP>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
 }
 
 // ---------------------------------------------------------------------------------
@@ -517,6 +538,11 @@ void launch_build_split(const Geo& g, double* const (&dst)[4][3], cudaStream_t s
   build_split_q<QUR>(g, dst[1], st);
   build_split_q<QUT>(g, dst[2], st);
   build_split_q<QUP>(g, dst[3], st);
+}
+
+void launch_react(const Geo& g, const double* ar, const double* at, double* rt, double* rp, cudaStream_t st) {
+  const dim3 grid((g.np + 1 + 127) / 128, g.nt + 1, g.npatch * g.nr);
+  k_react<<<grid, 128, 0, st>>>(g, ar, at, rt, rp);
 }
 
 }  // namespace yy

@@ -96,7 +96,8 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
   const long long po = patch * psize(g, K);
   const long long pc = patch * psize(g, KC);
   const int node = IX<K>(g, i, j, k);
-  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP)};
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
+          a.rt + patch * psize(g, KT), a.rp + patch * psize(g, KP)};
   const double* Wnew = a.wnew ? a.wnew + patch * 2 * wsize(g, K) : nullptr;
   const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
   Star x1 = load_star<K>(g, a.it + po, Wnew, i, j, k);
