@@ -37,18 +37,19 @@ template <int K>
 __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict__ F,
                                           const double* __restrict__ W, int i, int j, int k) {
   // read-only (non-coherent) loads: no kernel that calls this writes F or W
+  // one base pointer per node, neighbours at +-1 (immediate), +-st, +-sr
   Star s;
-  const int nd = IX<K>(g, i, j, k);
-  const int sr = NTk(g, K) * NPk(g, K), st = NPk(g, K);
-  s.c = __ldg(F + nd);
+  const double* p = F + IX<K>(g, i, j, k);
+  const int sr = SR<K>(g), st = ST<K>(g);
+  s.c = __ldg(p);
   if (K != KR && g.wall_lo && i == g.ilo_c) s.xm = 2.0 * __ldg(W + j * NPk(g, K) + k) - s.c;
-  else s.xm = __ldg(F + nd - sr);
+  else s.xm = __ldg(p - sr);
   if (K != KR && g.wall_hi && i == g.ihi_c) s.xp = 2.0 * __ldg(W + wsize(g, K) + j * NPk(g, K) + k) - s.c;
-  else s.xp = __ldg(F + nd + sr);
-  s.ym = __ldg(F + nd - st);
-  s.yp = __ldg(F + nd + st);
-  s.zm = __ldg(F + nd - 1);
-  s.zp = __ldg(F + nd + 1);
+  else s.xp = __ldg(p + sr);
+  s.ym = __ldg(p - st);
+  s.yp = __ldg(p + st);
+  s.zm = __ldg(p - 1);
+  s.zp = __ldg(p + 1);
   return s;
 }
 
@@ -106,17 +107,19 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
   double E = 0.0;
   if (Q == QUR) {
     // buoyancy +Pr Ra T^{n+1/2,(k)} e_r (RD20, RD21)
-    const double* Ti = a.Tit + pc;
-    const double* Tn = a.Tn + pc;
-    const double tb0 = 0.5 * (__ldg(Ti + IX<KC>(g, i - 1, j, k)) + __ldg(Tn + IX<KC>(g, i - 1, j, k)));
-    const double tb1 = 0.5 * (__ldg(Ti + IX<KC>(g, i, j, k)) + __ldg(Tn + IX<KC>(g, i, j, k)));
+    const int c0 = IX<KC>(g, i, j, k), src = SR<KC>(g);
+    const double* Ti = a.Tit + pc + c0;
+    const double* Tn = a.Tn + pc + c0;
+    const double tb0 = 0.5 * (__ldg(Ti - src) + __ldg(Tn - src));
+    const double tb1 = 0.5 * (__ldg(Ti) + __ldg(Tn));
     E = g.PrRa * 0.5 * (tb0 + tb1);
   } else if (Q == QUT) {
     // c_chi D21 ub_r + nu((2/r^2) d_th ub_r + (2 cos/(r^3 sin)) d_r(r^2 ub_r))  (eq:theta_comp)
     const long long orr = patch * psize(g, KR);
-    const double *uri = a.urit + orr, *urn = a.urn + orr;
-    auto ub = [&](int ii, int jj) {
-      const long long q = IX<KR>(g, ii, jj, k);
+    const int q0 = IX<KR>(g, i, j, k), srr = SR<KR>(g), str = ST<KR>(g);
+    const double *uri = a.urit + orr + q0, *urn = a.urn + orr + q0;
+    auto ub = [&](int ii, int jj) {     // (ii, jj) in {i, i+1} x {j-1, j}
+      const int q = (ii - i) * srr + (jj - j) * str;
       return 0.5 * (__ldg(uri + q) + __ldg(urn + q));
     };
     const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1), iv = __ldg(g.idv1_c + i);
@@ -129,13 +132,14 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
   } else if (Q == QUP) {
     // c_chi (D31 ub_r + D32 ub_th) + nu((2/(r^2 sin)) d_ph ub_r + (2cos/(r^2 sin^2)) d_ph ub_th)
     const long long orr = patch * psize(g, KR), ot = patch * psize(g, KT);
-    const double *uri = a.urit + orr, *urn = a.urn + orr, *uti = a.utit + ot, *utn = a.utn + ot;
-    auto ubr = [&](int ii, int kk) {
-      const long long q = IX<KR>(g, ii, j, kk);
+    const int qr = IX<KR>(g, i, j, k), qt = IX<KT>(g, i, j, k), srr = SR<KR>(g), stt = ST<KT>(g);
+    const double *uri = a.urit + orr + qr, *urn = a.urn + orr + qr, *uti = a.utit + ot + qt, *utn = a.utn + ot + qt;
+    auto ubr = [&](int ii, int kk) {    // (ii, kk) in {i, i+1} x {k-1, k}
+      const int q = (ii - i) * srr + (kk - k);
       return 0.5 * (__ldg(uri + q) + __ldg(urn + q));
     };
-    auto ubt = [&](int jj, int kk) {
-      const long long q = IX<KT>(g, i, jj, kk);
+    auto ubt = [&](int jj, int kk) {    // (jj, kk) in {j, j+1} x {k-1, k}
+      const int q = (jj - j) * stt + (kk - k);
       return 0.5 * (__ldg(uti + q) + __ldg(utn + q));
     };
     const double ir = __ldg(g.ir_c + i), is = __ldg(g.is_c + j), ct = __ldg(g.cot_c + j);
@@ -154,9 +158,10 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
   }
   if (S == 2 && Q != QT) {
     // -1/2 grad(p1^(k) - p1^n)   (RD18)
-    const double *pi_ = a.p1it + pc, *pn = a.p1n + pc;
+    const int c0 = IX<KC>(g, i, j, k);
+    const double *pi_ = a.p1it + pc + c0, *pn = a.p1n + pc + c0;
     auto dp = [&](int ii, int jj, int kk) {
-      const long long q = IX<KC>(g, ii, jj, kk);
+      const int q = (ii - i) * SR<KC>(g) + (jj - j) * ST<KC>(g) + (kk - k);
       return __ldg(pi_ + q) - __ldg(pn + q);
     };
     if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) * g.idr;
