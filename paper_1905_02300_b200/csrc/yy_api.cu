@@ -86,7 +86,6 @@ struct yy_ctx {
   double* astar[3] = {};
   double* G[NF] = {};
   double* R = nullptr;
-  double* C = nullptr;
   double* part = nullptr;
   int maxb = 0;
   double* red = nullptr;
@@ -1406,7 +1405,7 @@ extern "C" yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar
   if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
   SweepArgs w{};
   w.ar = d_ar; w.at = d_at; w.ap = d_ap;
-  w.R = d_x; w.C = ctx->C; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
+  w.R = d_x; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
   launch_sweep(ctx->g, QT, axis, 1, false, false, false, w, nullptr, 1, ctx->st);
   CK(cudaGetLastError());
   return YY_OK;

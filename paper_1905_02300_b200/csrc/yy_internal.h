@@ -52,7 +52,6 @@ struct SweepArgs {
   const double *ar, *at, *ap;
   const double *rt, *rp;
   double* R;                 // in: rhs, out: solution (non-final); slab r-sweep: x0
-  double* C;                 // unused
   double* psi;               // FINAL: psi += x
   double* part;              // FINAL: norm partials of this slot (2 * maxb)
   int maxb;

@@ -191,3 +191,26 @@ def test_errors_are_reported():
         sh.set_param(99, 1.0)
     with pytest.raises(YYError):
         sh.step(1, -1.0)
+
+
+def test_c1_full_config_ten_steps():
+    """BASELINE config C1 as specified (16x16x48 per patch, eq:Exact, Pr=1, Ra=100,
+    dt=1e-3, 10 steps): every step within the per-step bar, equal Schwarz counts."""
+    _pair(W.config("C1"), 10)
+
+
+def test_hundred_steps_within_drift_bar():
+    """BASELINE bar after 100 steps (<= 1e-9 relative), with equal Schwarz counts
+    on every step, on a reduced convection shell (noise-seeded, Ra = 1e4)."""
+    cfg = W.small("C3", 8, 14, 40)
+    wl = W.make_workload(cfg)
+    sh = _shell(cfg)
+    sh.load_workload(wl)
+    o = _oracle(cfg)
+    o.load_workload(wl)
+    for _ in range(100):
+        sh.step(1, cfg.tol)
+        o.step(1, cfg.tol)
+        assert sh.stats()[-1][0] == o.stats[-1][0], (len(o.stats), sh.stats()[-1], o.stats[-1])
+    e, where = _relerr(sh, o)
+    assert e <= 1e-9, (e, where)
