@@ -48,6 +48,7 @@ struct yy_ctx {
   double R1 = 1, R2 = 2, Pr = 1, Ra = 0, dt = 1e-3, chi = 1.0;
   int max_iters = 100, fixed_iters = 0;
   bool fuse = false;           // residual fused into the first sweep (YY_FUSE=1; measured slower on C3 so far)
+  bool use_graph = true;       // replay each step's Schwarz iteration as a CUDA graph (YY_GRAPH=0: off)
   // distribution: npatch = g.npatch local patches, global id of
   // local patch 0 = patch0.  mode 0: both patches here; 1: loopback pair (two
   // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
@@ -854,9 +855,39 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   const int kmax = ctx->fixed_iters > 0 ? ctx->fixed_iters : ctx->max_iters;
   int k = 0;
   double rho = INFINITY;
+  // One Schwarz iteration is the same launch sequence every time within a step
+  // (a*, G and the level pointers are fixed for the step): capture it once per
+  // step as a CUDA graph (single context on a user stream, not profiling) and
+  // replay it — the ~35 kernels then follow each other without per-launch gaps.
+  const bool graph = ctx->use_graph && cs.size() == 1 && ctx->mode == 0 && ctx->st != nullptr && !ctx->prof_on;
+  cudaGraphExec_t gexec = nullptr;
+  long long glaunches = 0;
+  if (graph) {
+    cudaGraph_t gr = nullptr;
+    const long long l0 = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    yy_status sc = exchange_fringe(cs);
+    if (sc == YY_OK) { flux_fix(cs, tol); sc = iter_solve(cs); }
+    if (sc == YY_OK) sc = reduce_group(cs);
+    if (sc == YY_OK)
+      sc = cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st) == cudaSuccess
+               ? YY_OK : YY_ECUDA;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->st, &gr);
+    if (sc != YY_OK) return sc;
+    CK(ec);
+    const cudaError_t ei = cudaGraphInstantiate(&gexec, gr, 0);
+    cudaGraphDestroy(gr);
+    CK(ei);
+    glaunches = ctx->launches - l0;
+    ctx->launches = l0;
+  }
   while (k < kmax) {
     ++k;
-    if (ctx->schwarz == 1) {                               // multiplicative: Yin, then Yang with Yin's k
+    if (graph) {
+      const cudaError_t el = cudaGraphLaunch(gexec, ctx->st);
+      if (el != cudaSuccess) { cudaGraphExecDestroy(gexec); CK(el); }
+      ctx->launches += glaunches;
+    } else if (ctx->schwarz == 1) {                        // multiplicative: Yin, then Yang with Yin's k
       for (int p = 0; p < 2; ++p) {
         TRY(exchange_fringe_to(cs, p));                    // O5 for patch p
         std::vector<yy_ctx*> cp = of_patch(cs, p);
@@ -868,12 +899,14 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
       flux_fix(cs, tol);                                   // Alg. 1 step 4 (optional)
       TRY(iter_solve(cs));                                 // O6-O9, local norms
     }
-    TRY(reduce_group(cs));                                 // O10
-    for (yy_ctx* c : cs) {
-      yy_ctx* ctx = c;
-      CK(cudaGetLastError());
+    if (!graph) {
+      TRY(reduce_group(cs));                               // O10
+      for (yy_ctx* c : cs) {
+        yy_ctx* ctx = c;
+        CK(cudaGetLastError());
+      }
+      CK(cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     }
-    CK(cudaMemcpyAsync(ctx->red_host, ctx->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     for (yy_ctx* c : cs) {
       yy_ctx* ctx = c;
       CK(cudaStreamSynchronize(c->st));
@@ -881,11 +914,13 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     }
     rho = ctx->red_host[0];
     if (ctx->red_host[1] != 0.0) {
+      if (gexec) cudaGraphExecDestroy(gexec);
       for (yy_ctx* c : cs) fail(c, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
       return YY_ESOLVER;
     }
     if (ctx->fixed_iters <= 0 && rho < tol) break;
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
   for (yy_ctx* c : cs) step_end(c);
   *iters = k;
   *rho_out = rho;
@@ -915,6 +950,7 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
   yy_ctx* ctx = new yy_ctx();
   if (const char* e = std::getenv("YY_FUSE")) ctx->fuse = (e[0] && e[0] != '0');
+  if (const char* e = std::getenv("YY_GRAPH")) ctx->use_graph = !(e[0] == '0');
   ctx->R1 = R1; ctx->R2 = R2; ctx->Pr = Pr; ctx->Ra = Ra; ctx->dt = dt;
   HostGeo h = host_geo(gr, R1, R2);
   Geo& g = ctx->g;

@@ -214,3 +214,31 @@ def test_hundred_steps_within_drift_bar():
         assert sh.stats()[-1][0] == o.stats[-1][0], (len(o.stats), sh.stats()[-1], o.stats[-1])
     e, where = _relerr(sh, o)
     assert e <= 1e-9, (e, where)
+
+
+def test_graph_replay_is_bitwise_the_stream_path():
+    """With a user stream the step replays each Schwarz iteration as a CUDA graph
+    (yy_api.cu step_group): same kernels, same order -> bit-identical to the
+    plain stream launches (no stream, or YY_GRAPH=0), and to the oracle bar."""
+    import os
+    import torch
+    cfg = W.small("C3", 10, 18, 50)
+    wl = W.make_workload(cfg)
+    out = []
+    for graph in ("1", "0"):
+        os.environ["YY_GRAPH"] = graph
+        try:
+            st = torch.cuda.Stream()
+            sh = _shell(cfg, stream=st.cuda_stream)
+            sh.load_workload(wl)
+            sh.step(3, cfg.tol)
+            torch.cuda.synchronize()
+            out.append(([sh.get_fields(p, 0, s) for p in range(2) for s in (1, 2)], sh.stats()))
+            sh.close()
+        finally:
+            os.environ.pop("YY_GRAPH", None)
+    (fa, sa), (fb, sb) = out
+    assert sa == sb
+    for a, b in zip(fa, fb):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
