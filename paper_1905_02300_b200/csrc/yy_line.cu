@@ -289,7 +289,7 @@ enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2, MODE_SLAB = 3 };
 // chunk arrays are 6 M registers): measured on B200 (C3), 96 registers for
 // chunks of <= 12 rows beat the unconstrained ~130 (occupancy over ILP)
 constexpr int line_minb(int M) {
-  return YY_LINE_MINB > 0 ? YY_LINE_MINB : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 3 : 2);
+  return YY_LINE_MINB > 0 ? YY_LINE_MINB : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 2 : 1);
 }
 
 template <int Q, int AX, int MODE, int S, int P, int M>
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
   // Out-of-range elements (ragged tile / padded rows) re-read a valid node and
   // become identity rows: no load sits behind a branch.
   constexpr int UPL = M / 4;              // phi: elements per thread per line (LN = 128 UPL)
-  static_assert(AX != 2 || M % 4 == 0, "phi chunks: M multiple of 4");
+  static_assert(AX != 2 || (M % 4 == 0 && P == 32), "phi tiles: one warp per line, M multiple of 4");
   int lt, c1, nlines, L0, stride, i0 = 0, j0 = 0, k0 = 0, nd0 = 0;
   __shared__ int s_i[AX == 2 ? NL : 1], s_j[AX == 2 ? NL : 1], s_nd[AX == 2 ? NL : 1];
   if (AX == 2) {
@@ -532,8 +532,8 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
     if (n <= 64) YY_L(8, 8);
     if (n <= 96) YY_L(16, 6);
     if (n <= 128) YY_L(16, 8);
-    if (n <= 256) YY_L(32, 8);
-    if (n <= 384) YY_L(32, 12);
+    if (n <= 256) YY_L(16, 16);
+    if (n <= 384) YY_L(16, 24);
     YY_L(32, 16);                                  // n <= 512 (checked at create)
   }
 #undef YY_L
