@@ -288,12 +288,14 @@ enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2, MODE_SLAB = 3 };
 // resident 128-thread blocks per SM the register allocation must allow (the
 // chunk arrays are 6 M registers): measured on B200 (C3), 96 registers for
 // chunks of <= 12 rows beat the unconstrained ~130 (occupancy over ILP)
-constexpr int line_minb(int M) {
-  return YY_LINE_MINB > 0 ? YY_LINE_MINB : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 2 : 1);
+constexpr int line_minb(int P, int M) {
+  return YY_LINE_MINB > 0 ? YY_LINE_MINB
+         : P > 32 ? (M <= 6 ? 5 : 4)      // multi-warp phi lines (part_solve3: 3 live arrays)
+                  : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 2 : 1);
 }
 
 template <int Q, int AX, int MODE, int S, int P, int M>
-__global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, ResidArgs ra) {
+__global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs a, ResidArgs ra) {
   constexpr bool FINAL = (MODE == MODE_FINAL);
   constexpr int K = kind_of(Q);
   constexpr int NL = 128 / P;
@@ -312,11 +314,14 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
   // Element u (< M) of this thread in the build / write-back phases:
   //  r/theta: line l = t % NL (consecutive threads = consecutive k, coalesced),
   //           rows e = c M + u of chunk c = t / NL (a thread walks its chunk);
-  //  phi:     line l = u / (M/4), row e = t + 128 (u % (M/4)) (coalesced along the line).
+  //  phi:     line l = u / UPL, row e = t + 128 (u % UPL), UPL = P M / 128 (coalesced
+  //           along the line).
   // Out-of-range elements (ragged tile / padded rows) re-read a valid node and
   // become identity rows: no load sits behind a branch.
-  constexpr int UPL = M / 4;              // phi: elements per thread per line (LN = 128 UPL)
-  static_assert(AX != 2 || (M % 4 == 0 && P == 32), "phi tiles: one warp per line, M multiple of 4");
+  constexpr int UPL = P * M / 128;        // phi: elements per thread per line (LN = 128 UPL)
+  static_assert(AX != 2 || (P % 32 == 0 && (P * M) % 128 == 0), "phi tiles: whole warps per line, 128 | P M");
+  static_assert(AX == 2 || P <= 32, "r/theta tiles: a line's chunks within one warp");
+  static_assert(P <= 32 || MODE != MODE_SLAB, "slab r-lines: one warp per line");
   int lt, c1, nlines, L0, stride, i0 = 0, j0 = 0, k0 = 0, nd0 = 0;
   __shared__ int s_i[AX == 2 ? NL : 1], s_j[AX == 2 ? NL : 1], s_nd[AX == 2 ? NL : 1];
   if (AX == 2) {
@@ -421,7 +426,50 @@ __global__ void __launch_bounds__(128, line_minb(M)) k_line(Geo g, SweepArgs a, 
       up[u] = UP[o + u];
       rh[u] = RH[o + u];
     }
-    if (MODE == MODE_SLAB) {
+    if constexpr (P > 32) {
+      // long phi lines: W = P/32 warps per line.  Each warp solves its segment
+      // with the couplings to the neighbour segments kept symbolic (part_solve3,
+      // as for radial slabs), x = x0 + xlo X_LO + xhi X_HI; the 2W boundary
+      // unknowns of the line (first / last row of every segment) are then
+      // eliminated by one thread, and every thread finishes its chunk.
+      constexpr int W = P / 32;
+      __shared__ double s_if[NL * W][6], s_lh[NL * W][2];
+      const int lane = threadIdx.x & 31, sg = threadIdx.x >> 5;   // segment (line sg / W)
+      part_solve3<32, M>(lo, up, rh, lane);
+      if (lane == 0) { s_if[sg][0] = rh[0]; s_if[sg][1] = lo[0]; s_if[sg][2] = up[0]; }
+      if (lane == 31) { s_if[sg][3] = rh[M - 1]; s_if[sg][4] = lo[M - 1]; s_if[sg][5] = up[M - 1]; }
+      __syncthreads();
+      if (threadIdx.x < NL) {
+        // a_s = first row, b_s = last row of segment s:
+        //   a_s = x0_f + xlo_f b_{s-1} + xhi_f a_{s+1},  b_s = x0_l + xlo_l b_{s-1} + xhi_l a_{s+1}
+        // forward: b_{s-1} = be + ga a_s  ->  a_s = p_s + q_s a_{s+1}; back: a_W = 0
+        const double(*f)[6] = s_if + threadIdx.x * W;
+        double p[W], q[W], bb[W], gg[W];
+        double be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < W; ++s2) {
+          const double d = 1.0 / (1.0 - f[s2][1] * ga);
+          p[s2] = (f[s2][0] + f[s2][1] * be) * d;
+          q[s2] = f[s2][2] * d;
+          bb[s2] = be;
+          gg[s2] = ga;
+          be = f[s2][3] + f[s2][4] * (be + ga * p[s2]);
+          ga = f[s2][4] * ga * q[s2] + f[s2][5];
+        }
+        double an = 0.0;                         // a_{s+1}
+#pragma unroll
+        for (int s2 = W - 1; s2 >= 0; --s2) {
+          const double as = p[s2] + q[s2] * an;
+          s_lh[threadIdx.x * W + s2][0] = bb[s2] + gg[s2] * as;   // b_{s-1} (0 for s = 0)
+          s_lh[threadIdx.x * W + s2][1] = an;
+          an = as;
+        }
+      }
+      __syncthreads();
+      const double XL = s_lh[sg][0], XH = s_lh[sg][1];
+#pragma unroll
+      for (int u = 0; u < M; ++u) RH[o + u] = rh[u] + lo[u] * XL + up[u] * XH;
+    } else if constexpr (MODE == MODE_SLAB) {
       part_solve3<P, M>(lo, up, rh, c);
 #pragma unroll
       for (int u = 0; u < M; ++u) {
@@ -522,9 +570,10 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
     if (n <= 128) YY_L(32, 4);
     if (n <= 256) YY_L(32, 8);
     if (n <= 384) YY_L(32, 12);
-    if (n <= 512) YY_L(32, 16);
-    if (n <= 768) YY_L(32, 24);
-    YY_L(32, 36);                                  // n <= 1152 (checked at create)
+    if (n <= 512) YY_L(128, 4);                    // longer lines: 4 warps per line
+    if (n <= 640) YY_L(128, 5);
+    if (n <= 768) YY_L(128, 6);
+    YY_L(128, 9);                                  // n <= 1152 (checked at create)
   } else {
     const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
     if (n <= 16) YY_L(4, 4);

@@ -92,6 +92,15 @@ def test_wide_phi_rows():
     _pair(cfg, 1)
 
 
+@pytest.mark.parametrize("nph", [450, 1100])
+def test_long_phi_lines_multiwarp(nph):
+    # phi lines longer than 384 rows are solved by 4 warps per line (segment
+    # solves with symbolic couplings + the per-line 8-unknown boundary system):
+    # every factor position (first / plain / final) of every quantity
+    cfg = W.small("C1", 3, 10, nph, Ra=30.0, dt=1e-3)
+    _pair(cfg, 1, wl=W.random_state(cfg, seed=5, amp=2.0))
+
+
 def test_fixed_iterations_mode():
     cfg = W.small("C1", 5, 12, 30, dt=1e-3)
     _pair(cfg, 2, oracle_kw={"fixed_iters": 3}, shell_kw={"fixed_iters": 3})
@@ -156,7 +165,7 @@ def test_line_solve_c4_reduced():
 @pytest.mark.parametrize("shape", [(30, 12, 36), (60, 12, 36), (90, 12, 36), (120, 12, 36), (250, 12, 36),
                                    (300, 12, 36), (5, 60, 180), (5, 100, 300), (4, 200, 600), (4, 300, 900),
                                    (3, 12, 100), (4, 16, 200), (3, 12, 300), (4, 20, 500), (3, 24, 700),
-                                   (3, 40, 1100)])
+                                   (3, 40, 1100), (3, 12, 385), (3, 12, 640), (3, 12, 1152)])
 def test_line_solve_every_chunking(shape):
     """One case per (P chunks, M rows) dispatch branch of the line solver
     (yy_line.cu), incl. ragged lines (rows past n are identity rows) and the
