@@ -58,6 +58,7 @@ struct yy_ctx {
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
   double* bsplit[4][3] = {};   // split-row tables (Geo::bsplit)
+  double* adv[4][3] = {};      // per-step transport-velocity row weights (Geo::adv)
   double* react_t = nullptr;   // Astar::rt, Astar::rp (per step)
   double* react_p = nullptr;
   double flux_a2 = 0.0, flux_area = 0.0;   // |a|^2 and |dOmega| of one patch (host geometry)
@@ -671,6 +672,7 @@ yy_status step_begin(yy_ctx* ctx) {
   {
     ProfScope ps(ctx, "react", 1);
     launch_react(g, ctx->astar[0], ctx->astar[1], ctx->react_t, ctx->react_p, st);
+    launch_adv(g, ctx->astar[0], ctx->astar[1], ctx->astar[2], ctx->adv, NPT, st);
   }
   // O3: static right-hand sides
   for (int q = 0; q < (ctx->heat_only ? 1 : 4); ++q) {
@@ -1116,6 +1118,12 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
       g.bsplit[q][ax] = ctx->bsplit[q][ax];
     }
   launch_build_split(g, ctx->bsplit, ctx->st);
+  for (int K = 0; K < 4; ++K)
+    for (int ax = 0; ax < 3; ++ax) {
+      if ((s = dalloc(ctx, &ctx->adv[K][ax], npatch * psize(g, K))) != YY_OK) { yy_destroy(ctx); return s; }
+      cudaMemset(ctx->adv[K][ax], 0, npatch * psize(g, K) * sizeof(double));
+      g.adv[K][ax] = ctx->adv[K][ax];
+    }
   if (cudaDeviceSynchronize() != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
   *out = ctx;
   return YY_OK;
@@ -1442,6 +1450,9 @@ extern "C" yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar
   SweepArgs w{};
   w.ar = d_ar; w.at = d_at; w.ap = d_ap;
   w.R = d_x; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
+  // the row weights of these a* (overwrites the context's per-step ones: the next
+  // yy_step recomputes them from its own a*)
+  launch_adv(ctx->g, d_ar, d_at, d_ap, ctx->adv, 1, ctx->st);
   launch_sweep(ctx->g, QT, axis, 1, false, false, false, w, nullptr, 1, ctx->st);
   CK(cudaGetLastError());
   return YY_OK;

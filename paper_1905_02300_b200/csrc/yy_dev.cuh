@@ -50,6 +50,8 @@ struct Geo {
   // [i][j][am, a0, ap] over the kind's (r, theta) nodes (k-independent), built once
   // on the device from coef<Q, AX, true, false> (yy_kernels.cu: k_build_split)
   const double* bsplit[4][3];
+  // per-step transport-velocity row weights by node kind and axis (k_adv; Astar::av)
+  const double* adv[4][3];
 };
 
 // 1/x to full fp64 precision (<= 1 ulp): hardware approximation refined by two
@@ -98,7 +100,20 @@ struct Astar {
   // abar_t<PH> cot(theta)) / r at u_phi nodes
   const double* __restrict__ rt;
   const double* __restrict__ rp;
+  // the transport-velocity row weights of the nodes of one kind, one per axis,
+  // evaluated once per step (k_adv; Geo::adv): av[d] = abar_d<K> (0.5 / h_d) times
+  // the axis' metric factor, i.e. the `adv` of coef<Q, d> (bind_adv)
+  const double* __restrict__ av[3] = {};
 };
+
+// Astar::av of kind K for patch `patch` (the RX paths of coef / coef_split read them)
+template <int K>
+__device__ __forceinline__ void bind_adv(const Geo& g, Astar& A, int patch) {
+  const long long o = patch * psize(g, K);
+  A.av[0] = g.adv[K][0] + o;
+  A.av[1] = g.adv[K][1] + o;
+  A.av[2] = g.adv[K][2] + o;
+}
 
 // a*_r averaged to the nodes of kind K (average along every axis where the
 // staggerings differ; SURVEY Appendix A "Advection").
@@ -153,6 +168,22 @@ template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {  
   return K == KT ? __ldg(g.cot_f + j) : __ldg(g.cot_c + j);
 }
 
+// Where the rows take the transport-velocity weight from the per-step arrays
+// Astar::av (RX = RX_SWEEP: line sweeps, RX_RESID: residuals; bit 3 Q + AX of the
+// masks) instead of averaging a* in place.  RX = 0 (static kernels): a* always.
+// Defaults measured on B200 (C3): every residual / sweep except the T residual
+// and the phi sweeps of T and u_r, whose in-place averages are as cheap.
+enum { RX_NONE = 0, RX_SWEEP = 1, RX_RESID = 2 };
+#ifndef YY_AV_SWEEP
+#define YY_AV_SWEEP 0xfdb
+#endif
+#ifndef YY_AV_RESID
+#define YY_AV_RESID 0xff8
+#endif
+__host__ __device__ constexpr bool use_av(int Q, int AX, int RX) {
+  return RX == RX_SWEEP ? ((YY_AV_SWEEP >> (3 * Q + AX)) & 1) : RX == RX_RESID ? ((YY_AV_RESID >> (3 * Q + AX)) & 1) : false;
+}
+
 // Row weights (am, a0, ap) of the directional operator L_{Q,AX} at node (i,j,k):
 //   (L X)_n = am X_{n-e} + a0 X_n + ap X_{n+e}.
 // HAT selects the implicit (split) operator with Delta^_thth, Delta^_phph
@@ -162,7 +193,7 @@ template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {  
 // RX: the reaction terms from the per-step arrays Astar::rt/rp (the sweeps) instead
 // of from the a* averages (the residual and static kernels, which load those a*
 // values for the other terms anyway).
-template <int Q, int AX, bool HAT, bool ADV = true, bool RX = false>
+template <int Q, int AX, bool HAT, bool ADV = true, int RX = 0>
 __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j, int k,
                                      double& am, double& a0, double& ap) {
   constexpr int K = kind_of(Q);
@@ -171,7 +202,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     // Delta_rr = (1/r^2) d_r(r^2 d_r), flux form; - a_r d_r
     const double dm = D * (K == KR ? __ldg(g.lr_fm + i) : __ldg(g.lr_cm + i));
     const double dp = D * (K == KR ? __ldg(g.lr_fp + i) : __ldg(g.lr_cp + i));
-    const double adv = ADV ? abar_r<K>(g, A, i, j, k) * (0.5 * g.idr) : 0.0;
+    const double adv = !ADV ? 0.0 : use_av(Q, 0, RX) ? __ldg(A.av[0] + IX<K>(g, i, j, k)) : abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
@@ -189,7 +220,9 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     const double rho = HAT ? g.iR1sq : ir2n<K>(g, i);
     const double dm = D * rho * (K == KT ? __ldg(g.lt_fm + j) : __ldg(g.lt_cm + j));
     const double dp = D * rho * (K == KT ? __ldg(g.lt_fp + j) : __ldg(g.lt_cp + j));
-    const double adv = ADV ? abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i) : 0.0;
+    const double adv = !ADV ? 0.0
+                       : use_av(Q, 1, RX) ? __ldg(A.av[1] + IX<K>(g, i, j, k))
+                            : abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
@@ -209,7 +242,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     // Delta_phph = d_phph/(r^2 sin^2 th); hat: 1/(R1^2 sin^2 th_1); - (a_ph/(r sin th)) d_ph
     const double ir = irn<K>(g, i), is = isn<K>(g, j);
     const double c = HAT ? D * g.hatph : D * ir2n<K>(g, i) * is2n<K>(g, j) * g.idph2;
-    const double adv = ADV ? abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is : 0.0;
+    const double adv = !ADV ? 0.0 : use_av(Q, 2, RX) ? __ldg(A.av[2] + IX<K>(g, i, j, k)) : abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is;
     am = c + adv;
     ap = c - adv;
     a0 = -2.0 * c;
@@ -232,7 +265,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
 // part (Geo::bsplit) + the transport-velocity terms: the same rows as
 // coef<Q,AX,true> up to the order of the additions, with 3 table loads instead of
 // the 1-D factor products.
-template <int Q, int AX, bool RX = false>
+template <int Q, int AX, int RX = 0>
 __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, int j, int k,
                                            double& am, double& a0, double& ap) {
   constexpr int K = kind_of(Q);
@@ -248,7 +281,11 @@ __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, 
   a0 = __ldg(b + 1);
   ap = __ldg(b + 2);
   double adv;
-  if (AX == 0) {
+  if (use_av(Q, AX, RX)) {
+    adv = __ldg(A.av[AX] + IX<K>(g, i, j, k));
+    if (AX == 1 && Q == QUT) a0 -= __ldg(A.rt + IX<KT>(g, i, j, k));
+    if (AX == 2 && Q == QUP) a0 -= __ldg(A.rp + IX<KP>(g, i, j, k));
+  } else if (AX == 0) {
     adv = abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
   } else if (AX == 1) {
     adv = abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);

@@ -427,6 +427,25 @@ __global__ void __launch_bounds__(128) k_react(Geo g, const double* __restrict__
         (abar_r<KP>(g, A, i, j, k) + abar_t<KP>(g, A, i, j, k) * __ldg(g.cot_c + j)) * __ldg(g.ir_c + i);
 }
 
+// per-step transport-velocity row weights (Astar::av) at the solved nodes of kind
+// K: the `adv` term of coef<Q, d> for d = r, theta, phi, the same expressions
+// (the sweeps and residuals then read one value per row instead of the a* averages)
+template <int K>
+__global__ void __launch_bounds__(128) k_adv(Geo g, const double* __restrict__ ar, const double* __restrict__ at,
+                                             const double* __restrict__ ap, double* __restrict__ d0,
+                                             double* __restrict__ d1, double* __restrict__ d2) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int patch = blockIdx.z / NRk(g, K);
+  const int i = blockIdx.z % NRk(g, K);
+  if (k >= NPk(g, K) || !solved<K>(g, i, j, k)) return;
+  const Astar A{ar + patch * psize(g, KR), at + patch * psize(g, KT), ap + patch * psize(g, KP), nullptr, nullptr};
+  const long long o = patch * psize(g, K) + IX<K>(g, i, j, k);
+  d0[o] = abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
+  d1[o] = abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
+  d2[o] = abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * irn<K>(g, i) * isn<K>(g, j);
+}
+
 // ---------------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------------
@@ -538,6 +557,14 @@ void launch_build_split(const Geo& g, double* const (&dst)[4][3], cudaStream_t s
   build_split_q<QUR>(g, dst[1], st);
   build_split_q<QUT>(g, dst[2], st);
   build_split_q<QUP>(g, dst[3], st);
+}
+
+void launch_adv(const Geo& g, const double* ar, const double* at, const double* ap, double* const (&dst)[4][3],
+                int npatch, cudaStream_t st) {
+  k_adv<KC><<<pgrid(g, KC, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KC][0], dst[KC][1], dst[KC][2]);
+  k_adv<KR><<<pgrid(g, KR, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KR][0], dst[KR][1], dst[KR][2]);
+  k_adv<KT><<<pgrid(g, KT, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KT][0], dst[KT][1], dst[KT][2]);
+  k_adv<KP><<<pgrid(g, KP, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KP][0], dst[KP][1], dst[KP][2]);
 }
 
 void launch_react(const Geo& g, const double* ar, const double* at, double* rt, double* rp, cudaStream_t st) {

@@ -121,24 +121,26 @@ __device__ __forceinline__ void part_solve(double (&lo)[M], double (&up)[M], dou
 
 __device__ __forceinline__ void pf_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
-// L1 prefetch of the a* values coef<Q,AX,true> reads at node (i,j,k) of kind K
-// (the neighbours along the line are the thread's / warp's other elements)
+// L1 prefetch of the per-step row weights coef<Q,AX,true> reads at node (i,j,k)
+// of kind K (Astar::av, and the reaction array of an own-direction row)
 template <int Q, int AX>
 __device__ __forceinline__ void prefetch_rows(const Geo& g, const Astar& A, int i, int j, int k) {
   constexpr int K = kind_of(Q);
-  if (AX == 0) {
+  if (use_av(Q, AX, RX_SWEEP)) {
+    pf_l1(A.av[AX] + IX<K>(g, i, j, k));
+  } else if (AX == 0) {
     pf_l1(A.ar + IX<KR>(g, i, j, k));
     if (K == KT) pf_l1(A.ar + IX<KR>(g, i, j - 1, k));
   } else if (AX == 1) {
     pf_l1(A.at + IX<KT>(g, i, j, k));
     if (K == KR) pf_l1(A.at + IX<KT>(g, i - 1, j, k));
-    if (Q == QUT) pf_l1(A.rt + IX<KT>(g, i, j, k));
   } else {
     pf_l1(A.ap + IX<KP>(g, i, j, k));
     if (K == KR) pf_l1(A.ap + IX<KP>(g, i - 1, j, k));
     if (K == KT) pf_l1(A.ap + IX<KP>(g, i, j - 1, k));
-    if (Q == QUP) pf_l1(A.rp + IX<KP>(g, i, j, k));
   }
+  if (Q == QUT && AX == 1) pf_l1(A.rt + IX<KT>(g, i, j, k));
+  if (Q == QUP && AX == 2) pf_l1(A.rp + IX<KP>(g, i, j, k));
 }
 
 // part_solve for a line that is one radial slab of a longer r-line (SURVEY
@@ -238,7 +240,7 @@ __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, in
   constexpr int K = kind_of(Q);
   const double th = 0.5 * g.tau;
   double am, a0, ap;
-  coef_split<Q, AX, true>(g, A, i, j, k, am, a0, ap);
+  coef_split<Q, AX, RX_SWEEP>(g, A, i, j, k, am, a0, ap);
   double di = 1.0 - th * a0;
   if (AX == 0 && K != KR) {          // antisymmetric wall ghost of the increment (RD23)
     if (m == 0 && g.wall_lo) di = 1.0 - th * (a0 - am);
@@ -308,8 +310,9 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   const int patch = (AX == 2) ? blockIdx.y : blockIdx.z;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : (AX == 1) ? NTk(g, K) - 2 : NPk(g, K) - 2;
   const long long po = patch * psize(g, K);
-  const Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
           a.rt + patch * psize(g, KT), a.rp + patch * psize(g, KP)};
+  bind_adv<K>(g, A, patch);
   double* __restrict__ R = a.R + po;
   // Element u (< M) of this thread in the build / write-back phases:
   //  r/theta: line l = t % NL (consecutive threads = consecutive k, coalesced),

@@ -53,18 +53,19 @@ __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict
   return s;
 }
 
-// sum_d L_{Q,d} applied to a star.
-template <int Q, bool HAT>
+// sum_d L_{Q,d} applied to a star.  RX: transport-velocity and reaction weights
+// from the per-step arrays (Astar::av / rt / rp, bound by the caller).
+template <int Q, bool HAT, int RX = RX_NONE>
 __device__ __forceinline__ double applyL(const Geo& g, const Astar& A, int i, int j, int k, const Star& s) {
   double am, a0, ap, acc;
-  if (HAT) coef_split<Q, 0>(g, A, i, j, k, am, a0, ap);
-  else coef<Q, 0, false>(g, A, i, j, k, am, a0, ap);
+  if (HAT) coef_split<Q, 0, RX>(g, A, i, j, k, am, a0, ap);
+  else coef<Q, 0, false, true, RX>(g, A, i, j, k, am, a0, ap);
   acc = am * s.xm + a0 * s.c + ap * s.xp;
-  if (HAT) coef_split<Q, 1>(g, A, i, j, k, am, a0, ap);
-  else coef<Q, 1, false>(g, A, i, j, k, am, a0, ap);
+  if (HAT) coef_split<Q, 1, RX>(g, A, i, j, k, am, a0, ap);
+  else coef<Q, 1, false, true, RX>(g, A, i, j, k, am, a0, ap);
   acc += am * s.ym + a0 * s.c + ap * s.yp;
-  if (HAT) coef_split<Q, 2>(g, A, i, j, k, am, a0, ap);
-  else coef<Q, 2, false>(g, A, i, j, k, am, a0, ap);
+  if (HAT) coef_split<Q, 2, RX>(g, A, i, j, k, am, a0, ap);
+  else coef<Q, 2, false, true, RX>(g, A, i, j, k, am, a0, ap);
   acc += am * s.zm + a0 * s.c + ap * s.zp;
   return acc;
 }
@@ -99,6 +100,7 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
   const int node = IX<K>(g, i, j, k);
   Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
           a.rt + patch * psize(g, KT), a.rp + patch * psize(g, KP)};
+  bind_adv<K>(g, A, patch);
   const double* Wnew = a.wnew ? a.wnew + patch * 2 * wsize(g, K) : nullptr;
   const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
   Star x1 = load_star<K>(g, a.it + po, Wnew, i, j, k);
@@ -168,7 +170,7 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) * (__ldg(g.ir_c + i) * g.idth);
     if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
   }
-  const double LX = applyL<Q, true>(g, A, i, j, k, X);
+  const double LX = applyL<Q, true, RX_RESID>(g, A, i, j, k, X);
   return __ldg(a.G + po + node) + g.tau * E - (X.c - 0.5 * g.tau * LX);
 }
 
