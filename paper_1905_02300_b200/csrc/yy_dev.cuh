@@ -173,7 +173,7 @@ template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {  
 // masks) instead of averaging a* in place.  RX = 0 (static kernels): a* always.
 // Defaults measured on B200 (C3): every residual / sweep except the T residual
 // and the phi sweeps of T and u_r, whose in-place averages are as cheap.
-enum { RX_NONE = 0, RX_SWEEP = 1, RX_RESID = 2 };
+enum { RX_NONE = 0, RX_SWEEP = 1, RX_RESID = 2, RX_GIVEN = 3 };   // GIVEN: adv / reaction passed in
 #ifndef YY_AV_SWEEP
 #define YY_AV_SWEEP 0xfdb
 #endif
@@ -195,14 +195,14 @@ __host__ __device__ constexpr bool use_av(int Q, int AX, int RX) {
 // values for the other terms anyway).
 template <int Q, int AX, bool HAT, bool ADV = true, int RX = 0>
 __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j, int k,
-                                     double& am, double& a0, double& ap) {
+                                     double& am, double& a0, double& ap, double advin = 0.0) {
   constexpr int K = kind_of(Q);
   const double D = (Q == QT) ? g.kap : g.nu;
   if (AX == 0) {
     // Delta_rr = (1/r^2) d_r(r^2 d_r), flux form; - a_r d_r
     const double dm = D * (K == KR ? __ldg(g.lr_fm + i) : __ldg(g.lr_cm + i));
     const double dp = D * (K == KR ? __ldg(g.lr_fp + i) : __ldg(g.lr_cp + i));
-    const double adv = !ADV ? 0.0 : use_av(Q, 0, RX) ? __ldg(A.av[0] + IX<K>(g, i, j, k)) : abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
+    const double adv = !ADV ? 0.0 : RX == RX_GIVEN ? advin : use_av(Q, 0, RX) ? __ldg(A.av[0] + IX<K>(g, i, j, k)) : abar_r<K>(g, A, i, j, k) * (0.5 * g.idr);
     am = dm + adv;
     ap = dp - adv;
     a0 = -(dm + dp);
@@ -221,6 +221,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     const double dm = D * rho * (K == KT ? __ldg(g.lt_fm + j) : __ldg(g.lt_cm + j));
     const double dp = D * rho * (K == KT ? __ldg(g.lt_fp + j) : __ldg(g.lt_cp + j));
     const double adv = !ADV ? 0.0
+                       : RX == RX_GIVEN ? advin
                        : use_av(Q, 1, RX) ? __ldg(A.av[1] + IX<K>(g, i, j, k))
                             : abar_t<K>(g, A, i, j, k) * (0.5 * g.idth) * irn<K>(g, i);
     am = dm + adv;
@@ -242,7 +243,7 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
     // Delta_phph = d_phph/(r^2 sin^2 th); hat: 1/(R1^2 sin^2 th_1); - (a_ph/(r sin th)) d_ph
     const double ir = irn<K>(g, i), is = isn<K>(g, j);
     const double c = HAT ? D * g.hatph : D * ir2n<K>(g, i) * is2n<K>(g, j) * g.idph2;
-    const double adv = !ADV ? 0.0 : use_av(Q, 2, RX) ? __ldg(A.av[2] + IX<K>(g, i, j, k)) : abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is;
+    const double adv = !ADV ? 0.0 : RX == RX_GIVEN ? advin : use_av(Q, 2, RX) ? __ldg(A.av[2] + IX<K>(g, i, j, k)) : abar_p<K>(g, A, i, j, k) * (0.5 * g.idph) * ir * is;
     am = c + adv;
     ap = c - adv;
     a0 = -2.0 * c;
@@ -267,13 +268,14 @@ __device__ __forceinline__ void coef(const Geo& g, const Astar& A, int i, int j,
 // the 1-D factor products.
 template <int Q, int AX, int RX = 0>
 __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, int j, int k,
-                                           double& am, double& a0, double& ap) {
+                                           double& am, double& a0, double& ap, double advin = 0.0,
+                                           double rxin = 0.0) {
   constexpr int K = kind_of(Q);
   // tabulated only where the own-direction row carries the metric / grad-div
   // terms (u_r in r, u_th in theta, u_ph in phi); measured on B200 (C3), the
   // plain Laplacian rows are cheaper from the 1-D factors
   if constexpr (!((Q == QUR && AX == 0) || (Q == QUT && AX == 1) || (Q == QUP && AX == 2))) {
-    coef<Q, AX, true, true, RX>(g, A, i, j, k, am, a0, ap);
+    coef<Q, AX, true, true, RX>(g, A, i, j, k, am, a0, ap, advin);
     return;
   }
   const double* b = g.bsplit[Q][AX] + 3 * (i * NTk(g, K) + j);
@@ -281,7 +283,10 @@ __device__ __forceinline__ void coef_split(const Geo& g, const Astar& A, int i, 
   a0 = __ldg(b + 1);
   ap = __ldg(b + 2);
   double adv;
-  if (use_av(Q, AX, RX)) {
+  if (RX == RX_GIVEN) {
+    adv = advin;
+    if ((AX == 1 && Q == QUT) || (AX == 2 && Q == QUP)) a0 -= rxin;
+  } else if (use_av(Q, AX, RX)) {
     adv = __ldg(A.av[AX] + IX<K>(g, i, j, k));
     if (AX == 1 && Q == QUT) a0 -= __ldg(A.rt + IX<KT>(g, i, j, k));
     if (AX == 2 && Q == QUP) a0 -= __ldg(A.rp + IX<KP>(g, i, j, k));

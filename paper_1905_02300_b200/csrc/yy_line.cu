@@ -120,6 +120,17 @@ __device__ __forceinline__ void part_solve(double (&lo)[M], double (&up)[M], dou
 }
 
 __device__ __forceinline__ void pf_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// 8-byte global -> shared copy that holds no register until it is waited for
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// axes (bit AX) whose build phase stages its inputs with cp.async; measured on
+// B200 (C3): faster for the phi tiles (one warp per line), slower for r / theta
+#ifndef YY_LINE_STAGE
+#define YY_LINE_STAGE 4
+#endif
 
 // L1 prefetch of the per-step row weights coef<Q,AX,true> reads at node (i,j,k)
 // of kind K (Astar::av, and the reaction array of an own-direction row)
@@ -234,13 +245,14 @@ __device__ __forceinline__ void part_solve3(double (&lo)[M], double (&up)[M], do
 }
 
 // normalised row m (0..n-1) of the factor at node (i,j,k); rv = right-hand side
-template <int Q, int AX>
+template <int Q, int AX, int RX = RX_SWEEP>
 __device__ __forceinline__ void make_row(const Geo& g, const Astar& A, int i, int j, int k, int m, int n,
-                                         double rv, double& lo, double& up, double& rh, bool keep_ends = false) {
+                                         double rv, double& lo, double& up, double& rh, bool keep_ends = false,
+                                         double advin = 0.0, double rxin = 0.0) {
   constexpr int K = kind_of(Q);
   const double th = 0.5 * g.tau;
   double am, a0, ap;
-  coef_split<Q, AX, RX_SWEEP>(g, A, i, j, k, am, a0, ap);
+  coef_split<Q, AX, RX>(g, A, i, j, k, am, a0, ap, advin, rxin);
   double di = 1.0 - th * a0;
   if (AX == 0 && K != KR) {          // antisymmetric wall ghost of the increment (RD23)
     if (m == 0 && g.wall_lo) di = 1.0 - th * (a0 - am);
@@ -380,6 +392,40 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       make_row<Q, AX>(g, A, i, j, k, ec, n, rv, lo, up, rh);
       const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
       const int s = slot(l, e);
+      LO[s] = lo * mk;
+      UP[s] = up * mk;
+      RH[s] = rh * mk;
+    }
+  } else if ((YY_LINE_STAGE >> AX) & 1) {
+    // every input value of the tile goes to shared memory with cp.async (no
+    // registers held, so all of a thread's loads are in flight at once): the
+    // right-hand side into the RH slot, the per-step row weight (Astar::av) into
+    // LO and the own-direction reaction into UP; the rows are then built in place
+    constexpr bool AVG = use_av(Q, AX, RX_SWEEP);
+    constexpr bool RXR = (Q == QUT && AX == 1) || (Q == QUP && AX == 2);
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      const int nd = node(l, min(e, n - 1), i, j, k);
+      const int s = slot(l, e);
+      cp_async8(RH + s, R + nd);
+      if (AVG) cp_async8(LO + s, A.av[AX] + nd);
+      else prefetch_rows<Q, AX>(g, A, i, j, k);
+      if (AVG && RXR) cp_async8(UP + s, (Q == QUT ? A.rt : A.rp) + nd);
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      const int ec = min(e, n - 1);
+      node(l, ec, i, j, k);
+      const int s = slot(l, e);
+      double lo, up, rh;
+      make_row<Q, AX, AVG ? RX_GIVEN : RX_SWEEP>(g, A, i, j, k, ec, n, RH[s], lo, up, rh, MODE == MODE_SLAB,
+                                                 AVG ? LO[s] : 0.0, (AVG && RXR) ? UP[s] : 0.0);
+      const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
       LO[s] = lo * mk;
       UP[s] = up * mk;
       RH[s] = rh * mk;
