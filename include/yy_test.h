@@ -24,9 +24,20 @@ yy_status yy_debug_get(yy_ctx* ctx, const char* name, int32_t patch, double* hos
  * velocity a* given by d_ar (nr+1,nt,np), d_at (nr,nt+1,np), d_ap (nr,nt,np+1)).
  * d_x (nr,nt,np) holds b on entry and x on exit at the solved nodes (fringe
  * layer untouched; homogeneous end conditions, wall ghost rule RD23).
- * All pointers are DEVICE pointers; asynchronous on ctx's stream. */
+ * All pointers are DEVICE pointers; asynchronous on ctx's stream.
+ * The rows' transport-velocity weights are first evaluated from a* (as
+ * yy_line_prepare); with d_ar = d_at = d_ap = NULL the a* and weights of the
+ * last yy_line_prepare are used instead (its a* arrays must still be valid; the
+ * per-step precompute of yy_step: a* fixed, many sweeps).  YY_EINVAL if only
+ * some of the three are NULL, YY_ESTATE if nothing was prepared. */
 yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar, const double* d_at,
                         const double* d_ap, double* d_x);
+
+/* Evaluate the temperature rows' transport-velocity weights of a* (device
+ * pointers, shapes as above) for later yy_line_solve calls with NULL a*.
+ * Overwrites the context's per-step weights (the next yy_step recomputes its
+ * own).  Asynchronous on ctx's stream. */
+yy_status yy_line_prepare(yy_ctx* ctx, const double* d_ar, const double* d_at, const double* d_ap);
 
 /* Two one-patch contexts in this process on the current device (out2[0] holds
  * Yin, out2[1] Yang) that exchange fringe values and norms by device copies on

@@ -59,6 +59,7 @@ struct yy_ctx {
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
   double* bsplit[4][3] = {};   // split-row tables (Geo::bsplit)
   double* adv[4][3] = {};      // per-step transport-velocity row weights (Geo::adv)
+  const double* line_a[3] = {};   // a* of the last yy_line_prepare
   double* react_t = nullptr;   // Astar::rt, Astar::rp (per step)
   double* react_p = nullptr;
   double flux_a2 = 0.0, flux_area = 0.0;   // |a|^2 and |dOmega| of one patch (host geometry)
@@ -1443,16 +1444,33 @@ yy_status yy_debug_get(yy_ctx* ctx, const char* name, int32_t patch, double* hos
 
 }  // extern "C"
 
+extern "C" yy_status yy_line_prepare(yy_ctx* ctx, const double* d_ar, const double* d_at, const double* d_ap) {
+  if (!ctx || !d_ar || !d_at || !d_ap) return YY_EINVAL;
+  if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  // the temperature rows' transport-velocity weights of these a* (patch 0; overwrites
+  // the context's per-step ones: the next yy_step recomputes them from its own a*)
+  launch_adv(ctx->g, d_ar, d_at, d_ap, ctx->adv, 1, ctx->st, 1 << KC);
+  ctx->line_a[0] = d_ar; ctx->line_a[1] = d_at; ctx->line_a[2] = d_ap;
+  CK(cudaGetLastError());
+  return YY_OK;
+}
+
 extern "C" yy_status yy_line_solve(yy_ctx* ctx, int32_t axis, const double* d_ar, const double* d_at,
                                    const double* d_ap, double* d_x) {
-  if (!ctx || axis < 0 || axis > 2 || !d_ar || !d_at || !d_ap || !d_x) return YY_EINVAL;
+  if (!ctx || axis < 0 || axis > 2 || !d_x) return YY_EINVAL;
+  const bool given = d_ar || d_at || d_ap;
+  if (given && !(d_ar && d_at && d_ap)) return YY_EINVAL;
   if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  if (given) {
+    yy_status s = yy_line_prepare(ctx, d_ar, d_at, d_ap);
+    if (s != YY_OK) return s;
+  } else if (!ctx->line_a[0]) {
+    return fail(ctx, YY_ESTATE, "yy_line_solve without a*: no yy_line_prepare before");
+  }
+  d_ar = ctx->line_a[0]; d_at = ctx->line_a[1]; d_ap = ctx->line_a[2];   // (rows that average a* in place)
   SweepArgs w{};
   w.ar = d_ar; w.at = d_at; w.ap = d_ap;
   w.R = d_x; w.psi = nullptr; w.part = nullptr; w.maxb = 0;
-  // the row weights of these a* (overwrites the context's per-step ones: the next
-  // yy_step recomputes them from its own a*)
-  launch_adv(ctx->g, d_ar, d_at, d_ap, ctx->adv, 1, ctx->st);
   launch_sweep(ctx->g, QT, axis, 1, false, false, false, w, nullptr, 1, ctx->st);
   CK(cudaGetLastError());
   return YY_OK;

@@ -119,10 +119,11 @@ struct InterpArgs {
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);
 // per step, after a*: the reaction coefficients rt (TH nodes), rp (PH nodes) of Astar
 void launch_react(const Geo& g, const double* ar, const double* at, double* rt, double* rp, cudaStream_t st);
-// per step, after a*: the transport-velocity row weights Astar::av of every kind
-// and axis (dst[K][d], at the solved nodes; Geo::adv points at them)
+// per step, after a*: the transport-velocity row weights Astar::av of the kinds in
+// the bit mask `kinds` and every axis (dst[K][d], at the solved nodes; Geo::adv
+// points at them)
 void launch_adv(const Geo& g, const double* ar, const double* at, const double* ap, double* const (&dst)[4][3],
-                int npatch, cudaStream_t st);
+                int npatch, cudaStream_t st, int kinds = 0xf);
 void launch_static(const Geo& g, int q, const StaticArgs& a, cudaStream_t st);
 void launch_resid(const Geo& g, int q, int s, const ResidArgs& a, cudaStream_t st);
 inline int max_line_len(int ax) { return ax == 2 ? 32 * 36 : 32 * 16; }   // unknowns per line (yy_line.cu)

@@ -560,11 +560,15 @@ void launch_build_split(const Geo& g, double* const (&dst)[4][3], cudaStream_t s
 }
 
 void launch_adv(const Geo& g, const double* ar, const double* at, const double* ap, double* const (&dst)[4][3],
-                int npatch, cudaStream_t st) {
-  k_adv<KC><<<pgrid(g, KC, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KC][0], dst[KC][1], dst[KC][2]);
-  k_adv<KR><<<pgrid(g, KR, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KR][0], dst[KR][1], dst[KR][2]);
-  k_adv<KT><<<pgrid(g, KT, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KT][0], dst[KT][1], dst[KT][2]);
-  k_adv<KP><<<pgrid(g, KP, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KP][0], dst[KP][1], dst[KP][2]);
+                int npatch, cudaStream_t st, int kinds) {
+  if (kinds & (1 << KC))
+    k_adv<KC><<<pgrid(g, KC, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KC][0], dst[KC][1], dst[KC][2]);
+  if (kinds & (1 << KR))
+    k_adv<KR><<<pgrid(g, KR, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KR][0], dst[KR][1], dst[KR][2]);
+  if (kinds & (1 << KT))
+    k_adv<KT><<<pgrid(g, KT, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KT][0], dst[KT][1], dst[KT][2]);
+  if (kinds & (1 << KP))
+    k_adv<KP><<<pgrid(g, KP, npatch), 128, 0, st>>>(g, ar, at, ap, dst[KP][0], dst[KP][1], dst[KP][2]);
 }
 
 void launch_react(const Geo& g, const double* ar, const double* at, double* rt, double* rp, cudaStream_t st) {

@@ -329,28 +329,27 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   // Element u (< M) of this thread in the build / write-back phases:
   //  r/theta: line l = t % NL (consecutive threads = consecutive k, coalesced),
   //           rows e = c M + u of chunk c = t / NL (a thread walks its chunk);
-  //  phi:     line l = u / UPL, row e = t + 128 (u % UPL), UPL = P M / 128 (coalesced
+  //  phi:     line l = t / P (P threads per line), row e = t % P + P u (coalesced
   //           along the line).
   // Out-of-range elements (ragged tile / padded rows) re-read a valid node and
   // become identity rows: no load sits behind a branch.
-  constexpr int UPL = P * M / 128;        // phi: elements per thread per line (LN = 128 UPL)
-  static_assert(AX != 2 || (P % 32 == 0 && (P * M) % 128 == 0), "phi tiles: whole warps per line, 128 | P M");
+  static_assert(AX != 2 || P % 32 == 0, "phi tiles: whole warps per line");
   static_assert(AX == 2 || P <= 32, "r/theta tiles: a line's chunks within one warp");
   static_assert(P <= 32 || MODE != MODE_SLAB, "slab r-lines: one warp per line");
   int lt, c1, nlines, L0, stride, i0 = 0, j0 = 0, k0 = 0, nd0 = 0;
-  __shared__ int s_i[AX == 2 ? NL : 1], s_j[AX == 2 ? NL : 1], s_nd[AX == 2 ? NL : 1];
-  if (AX == 2) {
+  // phi: the line of this thread (P threads per line) and its (i, j) and node at k = 1
+  int li = 0, lj = 0, lnd = 0;
+  auto line_of = [&](int t) {
     const int nj = NTk(g, K) - 2;
-    nlines = (i_hi<K>(g) - i_lo<K>(g) + 1) * nj;
+    const int L = min(L0 + t / P, nlines - 1);   // clamped: a ragged tile reads valid nodes
+    li = i_lo<K>(g) + L / nj;
+    lj = 1 + L % nj;
+    lnd = IX<K>(g, li, lj, 1);
+  };
+  if (AX == 2) {
+    nlines = (i_hi<K>(g) - i_lo<K>(g) + 1) * (NTk(g, K) - 2);
     L0 = blockIdx.x * NL;
-    if (threadIdx.x < NL) {
-      const int L = min(L0 + (int)threadIdx.x, nlines - 1);   // clamped: a ragged tile reads valid nodes
-      const int ii = i_lo<K>(g) + L / nj, jj = 1 + L % nj;
-      s_i[threadIdx.x] = ii;
-      s_j[threadIdx.x] = jj;
-      s_nd[threadIdx.x] = IX<K>(g, ii, jj, 1);
-    }
-    __syncthreads();
+    line_of(threadIdx.x);
     lt = 0;
     c1 = 0;
     stride = 1;
@@ -366,15 +365,15 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   }
   const bool lvalid = (AX == 2) || lt < nlines;
   auto elem = [&](int u, int& l, int& e) {
-    if (AX == 2) { l = u / UPL; e = threadIdx.x + 128 * (u % UPL); }
+    if (AX == 2) { l = threadIdx.x / P; e = threadIdx.x % P + P * u; }
     else { l = lt; e = c1 * M + u; }
   };
   auto exists = [&](int l, int e) { return e < n && (AX == 2 ? L0 + l < nlines : lvalid); };
   auto node = [&](int l, int e, int& i, int& j, int& k) {   // l, e clamped by the caller
     if (AX == 0) { i = i0 + e; j = j0; k = k0; return nd0 + e * stride; }
     if (AX == 1) { i = i0; j = j0 + e; k = k0; return nd0 + e * stride; }
-    i = s_i[l]; j = s_j[l]; k = 1 + e;
-    return s_nd[l] + e;
+    i = li; j = lj; k = 1 + e;
+    return lnd + e;
   };
   auto slot = [&](int l, int e) { return l * LP + (e / M) * MP + (e % M); };
   // 1. build
@@ -534,6 +533,12 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   }
   __syncthreads();
   // 4. write back
+  if (AX == 2) {
+    // recomputed (not kept live in registers across the solve)
+    int t = threadIdx.x;
+    asm volatile("" : "+r"(t));
+    line_of(t);
+  }
   double wsum = 0.0;
   double pv[M];
   if (FINAL) {

@@ -20,7 +20,7 @@ TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
            "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_time",
-           "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve", "yy_launch_count",
+           "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve", "yy_line_prepare", "yy_launch_count",
            "yy_profile_report")
 
 
@@ -74,6 +74,7 @@ def load_library():
     L.yy_destroy.restype = None
     L.yy_debug_get.argtypes = [ctx, c_char_p, c_int32, _DP]
     L.yy_line_solve.argtypes = [ctx, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
+    L.yy_line_prepare.argtypes = [ctx, c_void_p, c_void_p, c_void_p]
     L.yy_launch_count.argtypes = [ctx]
     L.yy_launch_count.restype = ctypes.c_int64
     L.yy_profile_report.argtypes = [ctx, ctypes.c_char_p, c_int32]
@@ -84,7 +85,7 @@ def load_library():
                                  c_int32, c_int32, c_void_p, c_int32, POINTER(ctx)]
     L.yy_nccl_unique_id.argtypes = [c_void_p]
     for name in ("yy_create_pair", "yy_create_slabs", "yy_create_dist", "yy_nccl_unique_id", "yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
-                 "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve",
+                 "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve", "yy_line_prepare",
                  "yy_profile_report"):
         getattr(L, name).restype = c_int32
     _lib = L
@@ -299,12 +300,21 @@ class Shell:
         return out
 
     def line_solve(self, axis, ar, at, ap, x):
-        """C4 kernel-only sweep on device tensors (torch, float64, contiguous)."""
+        """C4 kernel-only sweep on device tensors (torch, float64, contiguous).
+        ar = at = ap = None: the row weights of the last line_prepare."""
         for t in (ar, at, ap, x):
-            if not (t.is_cuda and t.dtype.is_floating_point and t.is_contiguous()):
+            if t is not None and not (t.is_cuda and t.dtype.is_floating_point and t.is_contiguous()):
                 raise YYError("line_solve needs contiguous CUDA float64 tensors")
-        self._check(self.L.yy_line_solve(self.h, axis, c_void_p(ar.data_ptr()), c_void_p(at.data_ptr()),
-                                         c_void_p(ap.data_ptr()), c_void_p(x.data_ptr())), "yy_line_solve")
+        p = lambda t: c_void_p(t.data_ptr()) if t is not None else None
+        self._check(self.L.yy_line_solve(self.h, axis, p(ar), p(at), p(ap), p(x)), "yy_line_solve")
+
+    def line_prepare(self, ar, at, ap):
+        """Row weights of a* for line_solve(axis, None, None, None, x)."""
+        for t in (ar, at, ap):
+            if not (t.is_cuda and t.dtype.is_floating_point and t.is_contiguous()):
+                raise YYError("line_prepare needs contiguous CUDA float64 tensors")
+        self._check(self.L.yy_line_prepare(self.h, c_void_p(ar.data_ptr()), c_void_p(at.data_ptr()),
+                                           c_void_p(ap.data_ptr())), "yy_line_prepare")
 
     def load_workload(self, wl):
         """Upload a workloads.make_workload() dict (levels, walls, sources)."""

@@ -188,6 +188,12 @@ def test_line_solve_every_chunking(shape):
         ref = o.sweep("T", rhs, axis, ops.coeffs(o.g, o.prm, "T", axis, True, astar))
         assert np.max(np.abs(got[m] - ref[m])) <= 1e-13 * np.max(np.abs(ref[m])), (shape, axis)
         assert np.array_equal(got[~m], rhs[~m]), (shape, axis)   # fringe untouched
+        # prepared row weights (yy_line_prepare + NULL a*): the same solve, bitwise
+        x2 = dev(rhs)
+        sh.line_prepare(dev(a["ur"]), dev(a["ut"]), dev(a["up"]))
+        sh.line_solve(axis, None, None, None, x2)
+        torch.cuda.synchronize()
+        assert np.array_equal(x2.cpu().numpy(), got), (shape, axis)
 
 
 def test_errors_are_reported():
