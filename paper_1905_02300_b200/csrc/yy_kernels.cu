@@ -132,17 +132,24 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
 // per thread (resid_at of yy_stencil.cuh).  The step normally fuses it into the
 // first sweep of each quantity (yy_line.cu) when YY_FUSE=1.
 // ---------------------------------------------------------------------------------
+// residual blocks: BK consecutive k x 128/BK consecutive j (the theta neighbours of
+// a column partly in the same block's L1); measured on B200 (C3): 64 for u_r,
+// 128 (one theta row) for the others
+#ifndef YY_RESID_BK
+#define YY_RESID_BK (Q == QUR ? 64 : 128)
+#endif
 template <int Q, int S, int IB>
 __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
   // thread = one (j, k) column, IB consecutive r-nodes (setup amortised, r-neighbours
   // of consecutive nodes shared through L1)
   constexpr int K = kind_of(Q);
-  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
-  const int j = blockIdx.y + 1;
+  constexpr int BK = YY_RESID_BK, BJ = 128 / BK;   // block = BK k x BJ j columns
+  const int k = blockIdx.x * BK + threadIdx.x % BK + 1;
+  const int j = blockIdx.y * BJ + threadIdx.x / BK + 1;
   const int nch = (i_hi<K>(g) - i_lo<K>(g) + IB) / IB;
   const int patch = blockIdx.z / nch;
   const int i0 = i_lo<K>(g) + (blockIdx.z % nch) * IB;
-  if (k > NPk(g, K) - 2) return;
+  if (k > NPk(g, K) - 2 || j > NTk(g, K) - 2) return;
   double* __restrict__ R = a.R + patch * psize(g, K);
 #pragma unroll
   for (int u = 0; u < IB; ++u) {
@@ -473,7 +480,8 @@ template <int Q, int S, int IB>
 void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   const int nch = (i_hi<K>(g) - i_lo<K>(g) + IB) / IB;
-  const dim3 grid((NPk(g, K) - 2 + 127) / 128, NTk(g, K) - 2, g.npatch * nch);
+  constexpr int BK = YY_RESID_BK, BJ = 128 / BK;
+  const dim3 grid((NPk(g, K) - 2 + BK - 1) / BK, (NTk(g, K) - 2 + BJ - 1) / BJ, g.npatch * nch);
   k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
 }
 // r-nodes per thread of the residual, per quantity (measured on B200, C3);
