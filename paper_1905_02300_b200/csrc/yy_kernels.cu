@@ -138,8 +138,11 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
 #ifndef YY_RESID_BK
 #define YY_RESID_BK (Q == QUR ? 64 : 128)
 #endif
+#ifndef YY_RESID_MINB
+#define YY_RESID_MINB 8
+#endif
 template <int Q, int S, int IB>
-__global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
+__global__ void __launch_bounds__(128, YY_RESID_MINB) k_resid(Geo g, ResidArgs a) {
   // thread = one (j, k) column, IB consecutive r-nodes (setup amortised, r-neighbours
   // of consecutive nodes shared through L1)
   constexpr int K = kind_of(Q);
@@ -151,10 +154,21 @@ __global__ void __launch_bounds__(128) k_resid(Geo g, ResidArgs a) {
   const int i0 = i_lo<K>(g) + (blockIdx.z % nch) * IB;
   if (k > NPk(g, K) - 2 || j > NTk(g, K) - 2) return;
   double* __restrict__ R = a.R + patch * psize(g, K);
+  // blocks away from the walls (all but the first / last chunk of r-nodes) take
+  // no wall-ghost code (a block-uniform branch)
+  const bool edge = K != KR && ((g.wall_lo && i0 == g.ilo_c) || (g.wall_hi && i0 + IB - 1 >= g.ihi_c));
+  if (edge) {
 #pragma unroll
-  for (int u = 0; u < IB; ++u) {
-    const int i = i0 + u;
-    if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S>(g, a, patch, i, j, k);
+    for (int u = 0; u < IB; ++u) {
+      const int i = i0 + u;
+      if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, true>(g, a, patch, i, j, k);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int i = i0 + u;
+      if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, false>(g, a, patch, i, j, k);
+    }
   }
 }
 

@@ -33,7 +33,8 @@ __device__ __forceinline__ Star star_lin(const Star& a, double fa, const Star& b
 // Star of field F (one patch) at (i,j,k).  For r-centred kinds the r
 // neighbours beyond the walls are the ghosts 2 w - psi_0 (reading RD22),
 // W = the field's wall data (2, NT, NP) at the matching time level.
-template <int K>
+// WALL = false: the caller knows (i,j,k) is no wall-adjacent node (no ghost code).
+template <int K, bool WALL = true>
 __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict__ F,
                                           const double* __restrict__ W, int i, int j, int k) {
   // read-only (non-coherent) loads: no kernel that calls this writes F or W
@@ -42,9 +43,9 @@ __device__ __forceinline__ Star load_star(const Geo& g, const double* __restrict
   const double* p = F + IX<K>(g, i, j, k);
   const int sr = SR<K>(g), st = ST<K>(g);
   s.c = __ldg(p);
-  if (K != KR && g.wall_lo && i == g.ilo_c) s.xm = 2.0 * __ldg(W + j * NPk(g, K) + k) - s.c;
+  if (WALL && K != KR && g.wall_lo && i == g.ilo_c) s.xm = 2.0 * __ldg(W + j * NPk(g, K) + k) - s.c;
   else s.xm = __ldg(p - sr);
-  if (K != KR && g.wall_hi && i == g.ihi_c) s.xp = 2.0 * __ldg(W + wsize(g, K) + j * NPk(g, K) + k) - s.c;
+  if (WALL && K != KR && g.wall_hi && i == g.ihi_c) s.xp = 2.0 * __ldg(W + wsize(g, K) + j * NPk(g, K) + k) - s.c;
   else s.xp = __ldg(p + sr);
   s.ym = __ldg(p - st);
   s.yp = __ldg(p + st);
@@ -92,7 +93,7 @@ __device__ __forceinline__ double div3(const Geo& g, const double* up, int i, in
 //   R = G + tau E_dyn - (I - tau/2 L_split)(psi~ - psi^n)
 // with the Gauss-Seidel dynamic terms E_dyn of SURVEY §8(c) O7/O9 (RD20, RD21,
 // RD18, RD-E1).
-template <int Q, int S>
+template <int Q, int S, bool WALL = true>
 __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int patch, int i, int j, int k) {
   constexpr int K = kind_of(Q);
   const long long po = patch * psize(g, K);
@@ -103,8 +104,8 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
   bind_adv<K>(g, A, patch);
   const double* Wnew = a.wnew ? a.wnew + patch * 2 * wsize(g, K) : nullptr;
   const double* Wn = a.wn ? a.wn + patch * 2 * wsize(g, K) : nullptr;
-  Star x1 = load_star<K>(g, a.it + po, Wnew, i, j, k);
-  Star x0 = load_star<K>(g, a.n + po, Wn, i, j, k);
+  Star x1 = load_star<K, WALL>(g, a.it + po, Wnew, i, j, k);
+  Star x0 = load_star<K, WALL>(g, a.n + po, Wn, i, j, k);
   Star X = star_lin(x1, 1.0, x0, -1.0);
   double E = 0.0;
   if (Q == QUR) {
