@@ -48,7 +48,9 @@ struct yy_ctx {
   double R1 = 1, R2 = 2, Pr = 1, Ra = 0, dt = 1e-3, chi = 1.0;
   int max_iters = 100, fixed_iters = 0;
   bool fuse = false;           // residual fused into the first sweep (YY_FUSE=1; measured slower on C3 so far)
-  bool use_graph = true;       // replay each step's Schwarz iteration as a CUDA graph (YY_GRAPH=0: off)
+  // 2: the whole Schwarz loop as one CUDA graph with a device-side WHILE node (one
+  // host sync per step); 1: each iteration as a graph, host-side loop; 0: streams
+  int use_graph = 2;           // YY_GRAPH=0/1/2
   // distribution: npatch = g.npatch local patches, global id of
   // local patch 0 = patch0.  mode 0: both patches here; 1: loopback pair (two
   // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
@@ -93,6 +95,7 @@ struct yy_ctx {
   int maxb = 0;
   double* red = nullptr;
   double* red_host = nullptr;   // pinned
+  double* ctl = nullptr;        // device-side Schwarz loop: iterations, rho, NaN flag
   double* wterm[2][MAXSRC][NW] = {};
   int nw[2] = {0, 0};
   int wtf[2][MAXSRC] = {};
@@ -865,6 +868,62 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   const bool graph = ctx->use_graph && cs.size() == 1 && ctx->mode == 0 && ctx->st != nullptr && !ctx->prof_on;
   cudaGraphExec_t gexec = nullptr;
   long long glaunches = 0;
+  if (graph && ctx->use_graph == 2) {
+    // the whole loop on the device: a WHILE node whose body is one iteration
+    // (O5-O10) followed by k_schwarz_cond; one launch and one host sync per step
+    const long long l0 = ctx->launches;
+    cudaGraph_t gr = nullptr;
+    CK(cudaGraphCreate(&gr, 0));
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&h, gr, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams np = {};
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) {
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      e = cudaGraphAddNode(&node, gr, nullptr, 0, &np);
+    }
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(ctx->st, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                            cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { cudaGraphDestroy(gr); CK(e); }
+    yy_status sc = exchange_fringe(cs);
+    if (sc == YY_OK) { flux_fix(cs, tol); sc = iter_solve(cs); }
+    if (sc == YY_OK) sc = reduce_group(cs);
+    if (sc == YY_OK) {
+      launch_schwarz_cond(h, ctx->red, ctx->ctl, tol, kmax, ctx->fixed_iters > 0, ctx->st);
+      ctx->launches += 1;
+    }
+    cudaGraph_t body = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->st, &body);
+    if (sc != YY_OK) { cudaGraphDestroy(gr); return sc; }
+    if (ec != cudaSuccess) { cudaGraphDestroy(gr); CK(ec); }
+    const long long per_iter = ctx->launches - l0;   // (incl. k_schwarz_cond)
+    ctx->launches = l0;
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&ge, gr, 0);
+    cudaGraphDestroy(gr);
+    CK(ei);
+    CK(cudaMemsetAsync(ctx->ctl, 0, 3 * sizeof(double), ctx->st));
+    const cudaError_t el = cudaGraphLaunch(ge, ctx->st);
+    if (el != cudaSuccess) { cudaGraphExecDestroy(ge); CK(el); }
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->ctl, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    const cudaError_t es = cudaStreamSynchronize(ctx->st);
+    cudaGraphExecDestroy(ge);
+    CK(es);
+    k = (int)ctx->red_host[0];
+    rho = ctx->red_host[1];
+    ctx->launches += per_iter * k;
+    if (ctx->red_host[2] != 0.0) {
+      fail(ctx, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
+      return YY_ESOLVER;
+    }
+    step_end(ctx);
+    *iters = k;
+    *rho_out = rho;
+    return YY_OK;
+  }
   if (graph) {
     cudaGraph_t gr = nullptr;
     const long long l0 = ctx->launches;
@@ -953,7 +1012,7 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
   yy_ctx* ctx = new yy_ctx();
   if (const char* e = std::getenv("YY_FUSE")) ctx->fuse = (e[0] && e[0] != '0');
-  if (const char* e = std::getenv("YY_GRAPH")) ctx->use_graph = !(e[0] == '0');
+  if (const char* e = std::getenv("YY_GRAPH")) ctx->use_graph = (e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
   ctx->R1 = R1; ctx->R2 = R2; ctx->Pr = Pr; ctx->Ra = Ra; ctx->dt = dt;
   HostGeo h = host_geo(gr, R1, R2);
   Geo& g = ctx->g;
@@ -1095,6 +1154,7 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if ((s = dalloc(ctx, &ctx->part, (size_t)NSLOT * 2 * mb)) != YY_OK || (s = dalloc(ctx, &ctx->red, 2 + 2 * NSLOT)) != YY_OK) { yy_destroy(ctx); return s; }
   cudaMemset(ctx->part, 0, (size_t)NSLOT * 2 * mb * sizeof(double));
   if (cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) { yy_destroy(ctx); return YY_ENOMEM; }
+  if ((s = dalloc(ctx, &ctx->ctl, 4)) != YY_OK) { yy_destroy(ctx); return s; }
   for (int L = 0; L < 3; ++L)
     for (int f = 0; f < NW; ++f)
       if ((s = dalloc(ctx, &ctx->wl[L][f], 2 * npatch * wsize(g, WKIND[f]))) != YY_OK) { yy_destroy(ctx); return s; }

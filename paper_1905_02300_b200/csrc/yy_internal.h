@@ -152,6 +152,10 @@ int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st);
 void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, cudaStream_t st);
 // rho = max over the 2 NSLOT sums -> out[0], NaN flag -> out[1]
 void launch_reduce_final(double* out, cudaStream_t st);
+// device-side Schwarz loop: ctl = {iterations, rho, NaN flag}; sets the WHILE
+// node's condition h (continue: no NaN, k < kmax, fixed or rho >= tol)
+void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double* ctl, double tol, int kmax,
+                         bool fixed, cudaStream_t st);
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st);
 // one patch per context: the donor evaluates the partner's fringe values from its
 // own patch into buf (pack), the target writes a received buf into its fringe

@@ -504,7 +504,7 @@ template <int Q, int S>
 void resid_q(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   static int ib[4] = {-1, -1, -1, -1};
   if (ib[0] < 0) {
-    const int def[4] = {4, 2, 2, 2};
+    const int def[4] = {2, 2, 2, 2};
     for (int q = 0; q < 4; ++q) ib[q] = def[q];
     if (const char* e = getenv("YY_RESID_IB")) sscanf(e, "%d,%d,%d,%d", &ib[0], &ib[1], &ib[2], &ib[3]);
   }
@@ -533,6 +533,27 @@ void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, c
 }
 
 void launch_reduce_final(double* out, cudaStream_t st) { k_reduce_final<<<1, 32, 0, st>>>(out); }
+
+// Device-side Schwarz loop control (the body's last node when the loop runs as a
+// conditional WHILE graph node): count the iteration, record rho and the NaN flag
+// (ctl[0..2]) and continue while no NaN, k < kmax and (fixed count or rho >= tol)
+// — the host loop's test (O10).
+__global__ void k_schwarz_cond(cudaGraphConditionalHandle h, const double* __restrict__ red,
+                               double* __restrict__ ctl, double tol, int kmax, int fixed) {
+  if (threadIdx.x == 0) {
+    const double k = ctl[0] + 1.0;
+    ctl[0] = k;
+    ctl[1] = red[0];
+    ctl[2] = red[1];
+    const bool more = red[1] == 0.0 && k < (double)kmax && (fixed || !(red[0] < tol));
+    cudaGraphSetConditional(h, more ? 1u : 0u);
+  }
+}
+
+void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double* ctl, double tol, int kmax,
+                         bool fixed, cudaStream_t st) {
+  k_schwarz_cond<<<1, 32, 0, st>>>(h, red, ctl, tol, kmax, fixed ? 1 : 0);
+}
 
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st) {
   if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 10), 128, 0, st>>>(g, a);

@@ -208,6 +208,30 @@ def test_errors_are_reported():
         sh.step(1, -1.0)
 
 
+@pytest.mark.parametrize("graph", ["2", "0"])
+def test_nan_state_is_reported(graph):
+    """A NaN in the state ends the Schwarz loop with YY_ESOLVER, on the
+    device-side loop (user stream, YY_GRAPH=2) as on the host loop."""
+    import os
+    import torch
+    from paper_1905_02300_b200 import YYError
+    cfg = W.small("C1", 4, 12, 28, dt=1e-3)
+    wl = W.make_workload(cfg)
+    os.environ["YY_GRAPH"] = graph
+    try:
+        st = torch.cuda.Stream()
+        sh = _shell(cfg, stream=st.cuda_stream)
+        sh.load_workload(wl)
+        T = wl["patches"][0]["n"]["T"].copy()
+        T[2, 5, 9] = np.nan
+        sh.set_fields(0, 0, 1, T=T)
+        with pytest.raises(YYError, match="NaN"):
+            sh.step(1, cfg.tol)
+        sh.close()
+    finally:
+        os.environ.pop("YY_GRAPH", None)
+
+
 def test_c1_full_config_ten_steps():
     """BASELINE config C1 as specified (16x16x48 per patch, eq:Exact, Pr=1, Ra=100,
     dt=1e-3, 10 steps): every step within the per-step bar, equal Schwarz counts."""
@@ -231,20 +255,23 @@ def test_hundred_steps_within_drift_bar():
     assert e <= 1e-9, (e, where)
 
 
-def test_graph_replay_is_bitwise_the_stream_path():
-    """With a user stream the step replays each Schwarz iteration as a CUDA graph
-    (yy_api.cu step_group): same kernels, same order -> bit-identical to the
-    plain stream launches (no stream, or YY_GRAPH=0), and to the oracle bar."""
+@pytest.mark.parametrize("fixed", [0, 4])
+def test_graph_replay_is_bitwise_the_stream_path(fixed):
+    """With a user stream the step runs the whole Schwarz loop as one CUDA graph
+    with a device-side WHILE node (YY_GRAPH=2, default) or replays each
+    iteration as a graph (YY_GRAPH=1) (yy_api.cu step_group): same kernels, same
+    order -> bit-identical to the plain stream launches (YY_GRAPH=0), with the
+    same iteration counts, to tolerance and with a fixed count."""
     import os
     import torch
     cfg = W.small("C3", 10, 18, 50)
     wl = W.make_workload(cfg)
     out = []
-    for graph in ("1", "0"):
+    for graph in ("2", "1", "0"):
         os.environ["YY_GRAPH"] = graph
         try:
             st = torch.cuda.Stream()
-            sh = _shell(cfg, stream=st.cuda_stream)
+            sh = _shell(cfg, stream=st.cuda_stream, **({"fixed_iters": fixed} if fixed else {}))
             sh.load_workload(wl)
             sh.step(3, cfg.tol)
             torch.cuda.synchronize()
@@ -252,8 +279,11 @@ def test_graph_replay_is_bitwise_the_stream_path():
             sh.close()
         finally:
             os.environ.pop("YY_GRAPH", None)
-    (fa, sa), (fb, sb) = out
-    assert sa == sb
-    for a, b in zip(fa, fb):
-        for k in a:
-            assert np.array_equal(a[k], b[k]), k
+    (fa, sa) = out[-1]
+    if fixed:
+        assert all(st[0] == fixed for st in sa), sa
+    for fb, sb in out[:-1]:
+        assert sa == sb
+        for a, b in zip(fa, fb):
+            for k in a:
+                assert np.array_equal(a[k], b[k]), k
