@@ -1,13 +1,19 @@
 # Round evidence on one B200: smoke, GPU tests, the default bench line, the ncu
 # launch list, and one `ncu --set full` capture of a whole Schwarz iteration's
 # hot kernels (summarised on the box: the report itself stays in /tmp), plus a
-# small full report of the dominant kernel.  LABEL names the build.
+# small full report of the dominant kernel.  LABEL names the build; NCU_ONLY=1
+# skips smoke / tests / bench.
 mkdir -p gpurun_out
 : > gpurun_out/rc.txt
 nvidia-smi > gpurun_out/smi.txt 2>&1
-python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/rc.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/rc.txt
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/rc.txt
+if [ -z "${NCU_ONLY:-}" ]; then
+  python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/rc.txt
+  timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/rc.txt
+  timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/rc.txt
+fi
+# ncu cannot profile the kernels of a graph with a conditional (WHILE) node: the
+# profiled runs replay each Schwarz iteration as a plain graph (same kernels)
+export YY_GRAPH=1
 B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
   -s 3000 -c 2500 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1
