@@ -366,8 +366,9 @@ def run_yy(args):
 
 def run_yy_dist(args, rank, world, local):
     """N = 2 nslab GPUs (yy_create_dist over NCCL): rank = patch * nslab + slab,
-    radial slabs of nr / nslab rows.  The workload is the N = 1 one, so the total
-    work is fixed: "scaling": "strong"."""
+    radial slabs of nr / nslab rows.  C1-C3: the workload is the N = 1 one, so the
+    total work is fixed ("scaling": "strong"); C5 (BASELINE's weak-scaling config):
+    patch Nr = 64 N, a fixed 128x192x576 shard per GPU ("scaling": "weak")."""
     import torch
     import torch.distributed as td
 
@@ -377,7 +378,8 @@ def run_yy_dist(args, rank, world, local):
     torch.cuda.set_device(local)
     td.init_process_group("nccl", device_id=torch.device("cuda", local))
     uid = dist.share_unique_id(rank, device=torch.device("cuda", local))
-    cfg = W.config(args.workload)
+    weak = args.workload == "C5"
+    cfg = W.config(args.workload, G=world) if weak else W.config(args.workload)
     wl = W.make_workload(cfg)
     stream = torch.cuda.Stream()
     dist.plan(world, rank, cfg.nr)                 # validates the slab split
@@ -411,7 +413,7 @@ def run_yy_dist(args, rank, world, local):
     if rank == 0:
         emit({"metric": METRIC, "value": 2 * cfg.cells * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
               "steps": args.steps, "warmup": W_, "ms_per_step": ms / args.steps, "higher_is_better": True,
-              "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+              "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
               "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
                          "parallelism": f"Yin on ranks 0..{world // 2 - 1}, Yang on the others, "
                                         f"{world // 2} radial slab(s) per patch; NCCL p2p fringe, halos, "
