@@ -51,6 +51,10 @@ struct yy_ctx {
   // 2: the whole Schwarz loop as one CUDA graph with a device-side WHILE node (one
   // host sync per step); 1: each iteration as a graph, host-side loop; 0: streams
   int use_graph = 2;           // YY_GRAPH=0/1/2
+  // alternate the block order of consecutive residual / sweep / pressure kernels
+  // (YY_ALT_ORDER=0: off); rev_next = the order of the next one
+  bool alt_order = true;
+  int rev_next = 0;
   // distribution: npatch = g.npatch local patches, global id of
   // local patch 0 = patch0.  mode 0: both patches here; 1: loopback pair (two
   // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
@@ -601,6 +605,13 @@ SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
   return w;
 }
 
+int next_order(yy_ctx* ctx) {
+  if (!ctx->alt_order) return 0;
+  const int r = ctx->rev_next;
+  ctx->rev_next ^= 1;
+  return r;
+}
+
 // O6/O7/O9 for one quantity on every context of the group: residual, the three
 // factor sweeps in the printed order (RD28) — the r-factor of radial slabs as the
 // partitioned solve across slabs — and the r-halos of the updated iterate
@@ -609,6 +620,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
   for (yy_ctx* ctx : cs) {
     if (ctx->fuse) continue;
     ResidArgs r = resid_args(ctx, q, s);
+    r.rev = next_order(ctx);
     ProfScope ps(ctx, kname(rname), 1);
     launch_resid(ctx->g, q, s, r, ctx->st);
   }
@@ -647,6 +659,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
     for (yy_ctx* ctx : cs) {
       ResidArgs r = resid_args(ctx, q, s);
       SweepArgs w = sweep_args(ctx, q, s, slot);
+      w.rev = next_order(ctx);
       ProfScope ps(ctx, kname(cls), 1);
       const int nb = launch_sweep(ctx->g, q, ax, s, first, fin, false, w, first ? &r : nullptr, ctx->g.npatch,
                                   ctx->st);
@@ -733,6 +746,7 @@ yy_status iter_solve(std::vector<yy_ctx*>& cs) {
       pa.pit = ctx->it[s == 1 ? FP1 : FP2];
       pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
       pa.maxb = ctx->maxb;
+      pa.rev = next_order(ctx);
       ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
       ctx->nblk[base + 3] = launch_pres(ctx->g, s, pa, ctx->st);
     }
@@ -1012,6 +1026,7 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
   yy_ctx* ctx = new yy_ctx();
   if (const char* e = std::getenv("YY_FUSE")) ctx->fuse = (e[0] && e[0] != '0');
+  if (const char* e = std::getenv("YY_ALT_ORDER")) ctx->alt_order = !(e[0] == '0');
   if (const char* e = std::getenv("YY_GRAPH")) ctx->use_graph = (e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
   ctx->R1 = R1; ctx->R2 = R2; ctx->Pr = Pr; ctx->Ra = Ra; ctx->dt = dt;
   HostGeo h = host_geo(gr, R1, R2);

@@ -90,6 +90,15 @@ __device__ __forceinline__ int IX(const Geo& g, int i, int j, int k) {
 template <int K> __host__ __device__ __forceinline__ int SR(const Geo& g) { return NTk(g, K) * NPk(g, K); }
 template <int K> __host__ __device__ __forceinline__ int ST(const Geo& g) { return NPk(g, K); }
 
+// Block index of a kernel whose blocks may run in reverse linear order: the
+// iteration alternates the order of consecutive kernels so that each starts on
+// the tiles the previous one touched last (still in L2).  Every block computes
+// the same tile either way (results are unchanged, bit for bit).
+__device__ __forceinline__ uint3 bidx(int rev) {
+  return rev ? make_uint3(gridDim.x - 1 - blockIdx.x, gridDim.y - 1 - blockIdx.y, gridDim.z - 1 - blockIdx.z)
+             : blockIdx;
+}
+
 // Transport velocity a* = u2^{*,n+1/2} (RD8), one patch.
 struct Astar {
   const double* __restrict__ ar;   // kind R

@@ -46,6 +46,7 @@ struct ResidArgs {
   const double *urit, *urn;  // this system's u_r (iterate, level n)
   const double *utit, *utn;
   const double *p1it, *p1n;
+  int rev;                   // reverse block order (bidx)
 };
 
 struct SweepArgs {
@@ -61,6 +62,7 @@ struct SweepArgs {
   double* V;
   double* W;
   double* IF;                // [line][6], line = (j-1)(np_k-2) + (k-1)
+  int rev;                   // run the grid's blocks in reverse linear order (bidx)
 };
 
 // one r-line's slab-coupling solution (yy_slab.cu)
@@ -77,6 +79,7 @@ struct PresArgs {
   double* pit;               // this system's p iterate (updated in place)
   double* part;
   int maxb;
+  int rev;                   // reverse block order (bidx)
 };
 
 // Algorithm 1 step 4 (mass-flux correction)

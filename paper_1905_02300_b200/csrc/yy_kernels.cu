@@ -143,15 +143,16 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
 #endif
 template <int Q, int S, int IB>
 __global__ void __launch_bounds__(128, YY_RESID_MINB) k_resid(Geo g, ResidArgs a) {
+  const uint3 B = bidx(a.rev);
   // thread = one (j, k) column, IB consecutive r-nodes (setup amortised, r-neighbours
   // of consecutive nodes shared through L1)
   constexpr int K = kind_of(Q);
   constexpr int BK = YY_RESID_BK, BJ = 128 / BK;   // block = BK k x BJ j columns
-  const int k = blockIdx.x * BK + threadIdx.x % BK + 1;
-  const int j = blockIdx.y * BJ + threadIdx.x / BK + 1;
+  const int k = B.x * BK + threadIdx.x % BK + 1;
+  const int j = B.y * BJ + threadIdx.x / BK + 1;
   const int nch = (i_hi<K>(g) - i_lo<K>(g) + IB) / IB;
-  const int patch = blockIdx.z / nch;
-  const int i0 = i_lo<K>(g) + (blockIdx.z % nch) * IB;
+  const int patch = B.z / nch;
+  const int i0 = i_lo<K>(g) + (B.z % nch) * IB;
   if (k > NPk(g, K) - 2 || j > NTk(g, K) - 2) return;
   double* __restrict__ R = a.R + patch * psize(g, K);
   // blocks away from the walls (all but the first / last chunk of r-nodes) take
@@ -177,10 +178,11 @@ __global__ void __launch_bounds__(128, YY_RESID_MINB) k_resid(Geo g, ResidArgs a
 // ---------------------------------------------------------------------------------
 template <int S>
 __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y;
+  const uint3 B = bidx(a.rev);
+  const int k = B.x * blockDim.x + threadIdx.x;
+  const int j = B.y;
   const int nz = (g.ihi_c - g.ilo_c + 4) / 4;
-  const int patch = blockIdx.z / nz, i0 = g.ilo_c + 4 * (blockIdx.z % nz);
+  const int patch = B.z / nz, i0 = g.ilo_c + 4 * (B.z % nz);
   double w = 0.0;
   if (k >= 1 && k <= g.np - 2 && j >= 1 && j <= g.nt - 2) {
     const long long pc = patch * psize(g, KC);
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
   }
   const double t = block_sum<128>(w);
   if (threadIdx.x == 0)
-    a.part[(long long)patch * a.maxb + ((blockIdx.z % nz) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    a.part[(long long)patch * a.maxb + ((B.z % nz) * gridDim.y + B.y) * gridDim.x + B.x] = t;
 }
 
 // ---------------------------------------------------------------------------------

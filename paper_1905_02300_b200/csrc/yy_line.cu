@@ -310,6 +310,7 @@ constexpr int line_minb(int P, int M) {
 
 template <int Q, int AX, int MODE, int S, int P, int M>
 __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs a, ResidArgs ra) {
+  const uint3 B = bidx(a.rev);
   constexpr bool FINAL = (MODE == MODE_FINAL);
   constexpr int K = kind_of(Q);
   constexpr int NL = 128 / P;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   double* LO = sm;
   double* UP = LO + NL * LP;
   double* RH = UP + NL * LP;
-  const int patch = (AX == 2) ? blockIdx.y : blockIdx.z;
+  const int patch = (AX == 2) ? B.y : B.z;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : (AX == 1) ? NTk(g, K) - 2 : NPk(g, K) - 2;
   const long long po = patch * psize(g, K);
   Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   };
   if (AX == 2) {
     nlines = (i_hi<K>(g) - i_lo<K>(g) + 1) * (NTk(g, K) - 2);
-    L0 = blockIdx.x * NL;
+    L0 = B.x * NL;
     line_of(threadIdx.x);
     lt = 0;
     c1 = 0;
@@ -356,11 +357,11 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   } else {
     lt = threadIdx.x % NL;
     c1 = threadIdx.x / NL;
-    L0 = blockIdx.x * NL + 1;             // first k of the tile
+    L0 = B.x * NL + 1;             // first k of the tile
     nlines = NPk(g, K) - 2 - L0 + 1;      // lines of this tile that exist (may exceed NL)
     k0 = L0 + min(lt, nlines - 1);
-    if (AX == 0) { i0 = i_lo<K>(g); j0 = blockIdx.y + 1; stride = NTk(g, K) * NPk(g, K); }
-    else { i0 = blockIdx.y + i_lo<K>(g); j0 = 1; stride = NPk(g, K); }
+    if (AX == 0) { i0 = i_lo<K>(g); j0 = B.y + 1; stride = NTk(g, K) * NPk(g, K); }
+    else { i0 = B.y + i_lo<K>(g); j0 = 1; stride = NPk(g, K); }
     nd0 = IX<K>(g, i0, j0, k0);
   }
   const bool lvalid = (AX == 2) || lt < nlines;
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = wsum;
     __syncthreads();
     if (threadIdx.x == 0) {
-      const int b = (AX == 2) ? blockIdx.x : blockIdx.y * gridDim.x + blockIdx.x;
+      const int b = (AX == 2) ? B.x : B.y * gridDim.x + B.x;
       a.part[(long long)patch * a.maxb + b] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
     }
   }

@@ -196,6 +196,32 @@ def test_line_solve_every_chunking(shape):
         assert np.array_equal(x2.cpu().numpy(), got), (shape, axis)
 
 
+def test_block_order_alternation_is_bitwise_neutral():
+    """Consecutive residual / sweep / pressure kernels run their blocks in
+    alternating linear order (L2 reuse, YY_ALT_ORDER): every block computes the
+    same tile and the norm partials keep their slots, so the step is bit-identical
+    with the alternation off."""
+    import os
+    cfg = W.small("C3", 9, 17, 47)
+    wl = W.random_state(cfg, seed=3, amp=1.0)
+    out = []
+    for alt in ("1", "0"):
+        os.environ["YY_ALT_ORDER"] = alt
+        try:
+            sh = _shell(cfg)
+            sh.load_workload(wl)
+            sh.step(2, cfg.tol)
+            out.append(([sh.get_fields(p, 0, s) for p in range(2) for s in (1, 2)], sh.stats()))
+            sh.close()
+        finally:
+            os.environ.pop("YY_ALT_ORDER", None)
+    (fa, sa), (fb, sb) = out
+    assert sa == sb
+    for a, b in zip(fa, fb):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+
+
 def test_errors_are_reported():
     from paper_1905_02300_b200 import YYError
     cfg = W.small("C1", 4, 12, 28)
