@@ -191,24 +191,37 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
     const double *uti = a.utit + ot, *utn = a.utn + ot;
     const double *upi = a.upit + op, *upn = a.upn + op;
     const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1), sn = __ldg(g.sc + j), is = __ldg(g.is_c + j);
-    for (int i = i0; i < i0 + 4 && i <= g.ihi_c; ++i) {
+    auto node = [&](int i) {
       const double ir = __ldg(g.ir_c + i);
       const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1);
-      const double ur0 = 0.5 * (uri[IX<KR>(g, i, j, k)] + urn[IX<KR>(g, i, j, k)]);
-      const double ur1 = 0.5 * (uri[IX<KR>(g, i + 1, j, k)] + urn[IX<KR>(g, i + 1, j, k)]);
-      const double ut0 = 0.5 * (uti[IX<KT>(g, i, j, k)] + utn[IX<KT>(g, i, j, k)]);
-      const double ut1 = 0.5 * (uti[IX<KT>(g, i, j + 1, k)] + utn[IX<KT>(g, i, j + 1, k)]);
-      const double up0 = 0.5 * (upi[IX<KP>(g, i, j, k)] + upn[IX<KP>(g, i, j, k)]);
-      const double up1 = 0.5 * (upi[IX<KP>(g, i, j, k + 1)] + upn[IX<KP>(g, i, j, k + 1)]);
+      const double ur0 = 0.5 * (__ldg(uri + IX<KR>(g, i, j, k)) + __ldg(urn + IX<KR>(g, i, j, k)));
+      const double ur1 = 0.5 * (__ldg(uri + IX<KR>(g, i + 1, j, k)) + __ldg(urn + IX<KR>(g, i + 1, j, k)));
+      const double ut0 = 0.5 * (__ldg(uti + IX<KT>(g, i, j, k)) + __ldg(utn + IX<KT>(g, i, j, k)));
+      const double ut1 = 0.5 * (__ldg(uti + IX<KT>(g, i, j + 1, k)) + __ldg(utn + IX<KT>(g, i, j + 1, k)));
+      const double up0 = 0.5 * (__ldg(upi + IX<KP>(g, i, j, k)) + __ldg(upn + IX<KP>(g, i, j, k)));
+      const double up1 = 0.5 * (__ldg(upi + IX<KP>(g, i, j, k + 1)) + __ldg(upn + IX<KP>(g, i, j, k + 1)));
       const double dv = (f1 * ur1 - f0 * ur0) * __ldg(g.idv1_c + i) + (s1 * ut1 - s0 * ut0) * (ir * is * g.idth) +
                         (up1 - up0) * (ir * is * g.idph);
       const long long q = pc + IX<KC>(g, i, j, k);
       double nv;
-      if (S == 1) nv = a.pn[q] - g.inv_chi * dv;
-      else nv = a.pn[q] + (a.p1it[q] - a.p1n[q]) - g.inv_chi * dv;
+      if (S == 1) nv = __ldg(a.pn + q) - g.inv_chi * dv;
+      else nv = __ldg(a.pn + q) + (__ldg(a.p1it + q) - __ldg(a.p1n + q)) - g.inv_chi * dv;
       const double d = nv - a.pit[q];
       a.pit[q] = nv;
       w += omega(g, __ldg(g.rc + i), sn) * d * d;
+    };
+    // 4 r-nodes per thread; system 1 unrolled (all loads of the four nodes in
+    // flight before the first update), system 2 (more arrays per node, already
+    // enough loads in flight) rolled at 32 registers — measured on B200 (C3)
+    if constexpr (S == 1) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + u > g.ihi_c) break;
+        node(i0 + u);
+      }
+    } else {
+#pragma unroll 1
+      for (int i = i0; i < i0 + 4 && i <= g.ihi_c; ++i) node(i);
     }
   }
   const double t = block_sum<128>(w);
