@@ -278,44 +278,85 @@ __device__ __forceinline__ double interp16(const Geo& g, int K, const double* __
   return v;
 }
 
+// the same with the 8 weights in registers and read-only donor loads
+__device__ __forceinline__ double interp16r(const double* __restrict__ base, int NP, const double (&w)[8]) {
+  double v = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double* row = base + a * NP;
+    const double s = w[4] * __ldg(row) + w[5] * __ldg(row + 1) + w[6] * __ldg(row + 2) + w[7] * __ldg(row + 3);
+    v += w[a] * s;
+  }
+  return v;
+}
+
+// r-levels per thread of the interpolation kernels: the entry's stencil (base
+// indices, weights, rotation) is read once and reused for IL levels
+constexpr int IL = 4;
+
 // scalar-like quantities on the (theta_c, phi_c) lattice: T, p1, p2, u_r1, u_r2
-// grid: x -> entry, y -> i (0..nr), z -> patch*5 + quantity
+// grid: x -> entry, y -> group of IL r-levels (0..nr), z -> patch*5 + quantity
 __global__ void k_interp_cc(Geo g, InterpArgs a) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
   const int patch = blockIdx.z / 5, q = blockIdx.z % 5;
   if (e >= a.tab_cc.n) return;
   const int K = (q < 3) ? KC : KR;
-  if (K == KC && (i < g.ifr_c0 || i > g.ifr_c1)) return;
-  if (K == KR && (i < g.ifr_f0 || i > g.ifr_f1)) return;
+  const int lo = K == KC ? g.ifr_c0 : g.ifr_f0, hi = K == KC ? g.ifr_c1 : g.ifr_f1;
+  const int i0 = max(lo, (int)blockIdx.y * IL);
+  const int i1 = min(hi, (int)blockIdx.y * IL + IL - 1);
+  if (i0 > i1) return;
   const long long ps = psize(g, K);
   double* X = a.cc[q];
-  const double* donor = X + (1 - patch) * ps;
-  double* tgt = X + patch * ps;
+  const int NT = NTk(g, K), NP = NPk(g, K);
   const int jb = a.tab_cc.jb[e], kb = a.tab_cc.kb[e];
-  const double v = interp16(g, K, donor, i, jb, kb, a.tab_cc.w + 8LL * e);
-  tgt[((long long)i * NTk(g, K) + a.tab_cc.tj[e]) * NPk(g, K) + a.tab_cc.tk[e]] = v;
+  double w[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) w[m] = __ldg(a.tab_cc.w + 8LL * e + m);
+  const double* donor = X + (1 - patch) * ps + (jb * NP + kb);
+  double* tgt = X + patch * ps + (a.tab_cc.tj[e] * NP + a.tab_cc.tk[e]);
+  const int sr = NT * NP;
+  double v[IL];
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1) v[u] = interp16r(donor + (long long)(i0 + u) * sr, NP, w);
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1) tgt[(long long)(i0 + u) * sr] = v[u];
 }
 
 // tangential vector components: target kind KT (u_th) or KP (u_ph) of both
 // systems; both donor components interpolated on their own lattices, rotated.
-// grid: x -> entry, y -> i, z -> patch*2 + system
+// grid: x -> entry, y -> group of IL r-levels, z -> patch*2 + system
 template <int KTGT>
 __global__ void k_interp_vec(Geo g, InterpArgs a) {
   const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
   const int patch = blockIdx.z / 2, s = blockIdx.z % 2;
-  if (e >= t.n || i < g.ifr_c0 || i > g.ifr_c1) return;
-  const double* ut = a.ut[s];
-  const double* up = a.up[s];
-  const double* dut = ut + (1 - patch) * psize(g, KT);
-  const double* dup = up + (1 - patch) * psize(g, KP);
-  const double vt = interp16(g, KT, dut, i, t.jb_t[e], t.kb_t[e], t.w_t + 8LL * e);
-  const double vp = interp16(g, KP, dup, i, t.jb_p[e], t.kb_p[e], t.w_p + 8LL * e);
-  const double v = t.m0[e] * vt + t.m1[e] * vp;
-  double* tgt = (KTGT == KT ? a.ut[s] : a.up[s]) + patch * psize(g, KTGT);
-  tgt[((long long)i * NTk(g, KTGT) + t.tj[e]) * NPk(g, KTGT) + t.tk[e]] = v;
+  const int i0 = max(g.ifr_c0, (int)blockIdx.y * IL);
+  const int i1 = min(g.ifr_c1, (int)blockIdx.y * IL + IL - 1);
+  if (e >= t.n || i0 > i1) return;
+  const int NPT = NPk(g, KT), NPP = NPk(g, KP);
+  const long long srt = (long long)NTk(g, KT) * NPT, srp = (long long)NTk(g, KP) * NPP;
+  const double* dut = a.ut[s] + (1 - patch) * psize(g, KT) + (t.jb_t[e] * NPT + t.kb_t[e]);
+  const double* dup = a.up[s] + (1 - patch) * psize(g, KP) + (t.jb_p[e] * NPP + t.kb_p[e]);
+  double wt[8], wp[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    wt[m] = __ldg(t.w_t + 8LL * e + m);
+    wp[m] = __ldg(t.w_p + 8LL * e + m);
+  }
+  const double m0 = t.m0[e], m1 = t.m1[e];
+  const int NPG = NPk(g, KTGT);
+  const long long srg = (long long)NTk(g, KTGT) * NPG;
+  double* tgt = (KTGT == KT ? a.ut[s] : a.up[s]) + patch * psize(g, KTGT) + (t.tj[e] * NPG + t.tk[e]);
+  double v[IL];
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1)
+      v[u] = m0 * interp16r(dut + (i0 + u) * srt, NPT, wt) + m1 * interp16r(dup + (i0 + u) * srp, NPP, wp);
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1) tgt[(i0 + u) * srg] = v[u];
 }
 
 // ---- one patch per context: donor-side evaluation + transfer + target write ----
@@ -571,9 +612,10 @@ void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double
 }
 
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st) {
-  if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 10), 128, 0, st>>>(g, a);
-  if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, g.nr, 4), 128, 0, st>>>(g, a);
-  if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 4), 128, 0, st>>>(g, a);
+  const int ngc = (g.nr + 1 + IL - 1) / IL, ngv = (g.nr + IL - 1) / IL;
+  if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 10), 128, 0, st>>>(g, a);
+  if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, ngv, 4), 128, 0, st>>>(g, a);
+  if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, ngv, 4), 128, 0, st>>>(g, a);
 }
 
 long long fringe_count(const Geo& g, const InterpArgs& a) {
