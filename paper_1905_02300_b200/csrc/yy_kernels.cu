@@ -233,14 +233,24 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
 // K6: deterministic final reduction: 18 (quantity, patch) sums in fixed order,
 // rho = max sqrt; NaN/Inf -> flag.
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_reduce_slots(const double* __restrict__ part, ReduceArgs a,
+__global__ void __launch_bounds__(512) k_reduce_slots(const double* __restrict__ part, ReduceArgs a,
                                                       double* __restrict__ out) {
   const int slot = blockIdx.x / a.npatch, lp = blockIdx.x % a.npatch;   // one block per (slot, local patch)
   const double* p = part + ((long long)slot * 2 + lp) * a.maxb;
   const int nb = a.nblk[slot];
-  double v = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += p[b];
-  const double t = block_sum<256>(v);
+  // four independent accumulators per thread (fixed assignment: loads in flight
+  // together), then a fixed tree
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  constexpr int NT = 512;
+  int b = threadIdx.x;
+  for (; b + 3 * NT < nb; b += 4 * NT) {
+    v0 += __ldg(p + b);
+    v1 += __ldg(p + b + NT);
+    v2 += __ldg(p + b + 2 * NT);
+    v3 += __ldg(p + b + 3 * NT);
+  }
+  for (; b < nb; b += NT) v0 += __ldg(p + b);
+  const double t = block_sum<NT>((v0 + v1) + (v2 + v3));
   if (threadIdx.x == 0) out[2 + 2 * slot + lp + a.patch0] = t;
 }
 
@@ -585,7 +595,7 @@ int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st) {
 }
 
 void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, cudaStream_t st) {
-  k_reduce_slots<<<a.npatch * NSLOT, 256, 0, st>>>(part, a, out);
+  k_reduce_slots<<<a.npatch * NSLOT, 512, 0, st>>>(part, a, out);
 }
 
 void launch_reduce_final(double* out, cudaStream_t st) { k_reduce_final<<<1, 32, 0, st>>>(out); }
