@@ -403,16 +403,33 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     // LO and the own-direction reaction into UP; the rows are then built in place
     constexpr bool AVG = use_av(Q, AX, RX_SWEEP);
     constexpr bool RXR = (Q == QUT && AX == 1) || (Q == QUP && AX == 2);
+    // phi: per-thread line base pointers and 32-bit row offsets (immediates for
+    // the unrolled elements); rows past the line end are zero-filled, not loaded
+    const double* __restrict__ Rb = R + lnd;
+    const double* __restrict__ Vb = A.av[AX] + lnd;
+    const double* __restrict__ Xb = (Q == QUT ? A.rt : A.rp) + lnd;
 #pragma unroll
     for (int u = 0; u < M; ++u) {
       int l, e, i, j, k;
       elem(u, l, e);
-      const int nd = node(l, min(e, n - 1), i, j, k);
       const int s = slot(l, e);
-      cp_async8(RH + s, R + nd);
-      if (AVG) cp_async8(LO + s, A.av[AX] + nd);
-      else prefetch_rows<Q, AX>(g, A, i, j, k);
-      if (AVG && RXR) cp_async8(UP + s, (Q == QUT ? A.rt : A.rp) + nd);
+      if (AX == 2 && AVG) {
+        if (e < n) {
+          cp_async8(RH + s, Rb + e);
+          cp_async8(LO + s, Vb + e);
+          if (RXR) cp_async8(UP + s, Xb + e);
+        } else {
+          RH[s] = 0.0;
+          LO[s] = 0.0;
+          UP[s] = 0.0;
+        }
+      } else {
+        const int nd = node(l, min(e, n - 1), i, j, k);
+        cp_async8(RH + s, R + nd);
+        if (AVG) cp_async8(LO + s, A.av[AX] + nd);
+        else prefetch_rows<Q, AX>(g, A, i, j, k);
+        if (AVG && RXR) cp_async8(UP + s, (Q == QUT ? A.rt : A.rp) + nd);
+      }
     }
     cp_async_wait_all();
 #pragma unroll
@@ -542,6 +559,35 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
   }
   double wsum = 0.0;
   double pv[M];
+  if constexpr (AX == 2 && MODE != MODE_SLAB) {
+    // phi: line base pointers, 32-bit row offsets, predicated (not clamped) rows
+    double* __restrict__ Pw = a.psi + po + lnd;
+    double* __restrict__ Rw = R + lnd;
+    const bool lv = L0 + (int)threadIdx.x / P < nlines;
+    if (FINAL) {
+#pragma unroll
+      for (int u = 0; u < M; ++u) {
+        int l, e;
+        elem(u, l, e);
+        pv[u] = (e < n) ? Pw[e] : 0.0;
+      }
+    }
+    const double rs = FINAL ? rnode<K>(g, li) * rnode<K>(g, li) * snode<K>(g, lj) : 0.0;
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e;
+      elem(u, l, e);
+      if (lv && e < n) {
+        const double x = RH[slot(l, e)];
+        if (FINAL) {
+          Pw[e] = pv[u] + x;
+          wsum += rs * x * x;
+        } else {
+          Rw[e] = x;
+        }
+      }
+    }
+  } else {
   if (FINAL) {
 #pragma unroll
     for (int u = 0; u < M; ++u) {
@@ -576,6 +622,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
         R[nd] = x;
       }
     }
+  }
   }
   if (FINAL) {
     wsum *= g.dr * g.dth * g.dph;
