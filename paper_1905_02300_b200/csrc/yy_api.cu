@@ -100,6 +100,7 @@ struct yy_ctx {
   double* red = nullptr;
   double* red_host = nullptr;   // pinned
   double* ctl = nullptr;        // device-side Schwarz loop: iterations, rho, NaN flag
+  double* dp1 = nullptr;        // p1^(k) - p1^n, both patches (two-patch contexts; NULL otherwise)
   double* wterm[2][MAXSRC][NW] = {};
   int nw[2] = {0, 0};
   int wtf[2][MAXSRC] = {};
@@ -591,6 +592,7 @@ ResidArgs resid_args(yy_ctx* ctx, int q, int s) {
   r.urit = ctx->it[FUR1 + o]; r.urn = ctx->n[FUR1 + o];
   r.utit = ctx->it[FUT1 + o]; r.utn = ctx->n[FUT1 + o];
   r.p1it = ctx->it[FP1]; r.p1n = ctx->n[FP1];
+  r.dp1 = (s == 2) ? ctx->dp1 : nullptr;
   return r;
 }
 
@@ -720,6 +722,7 @@ InterpArgs interp_args(yy_ctx* ctx) {
   ia.ut[0] = ctx->it[FUT1]; ia.ut[1] = ctx->it[FUT2];
   ia.up[0] = ctx->it[FUP1]; ia.up[1] = ctx->it[FUP2];
   ia.tab_cc = ctx->tcc; ia.tab_th = ctx->tth; ia.tab_ph = ctx->tph;
+  ia.dp1 = ctx->dp1; ia.p1n = ctx->n[FP1];
   return ia;
 }
 
@@ -746,6 +749,7 @@ yy_status iter_solve(std::vector<yy_ctx*>& cs) {
       pa.pit = ctx->it[s == 1 ? FP1 : FP2];
       pa.part = ctx->part + (long long)(base + 3) * 2 * ctx->maxb;
       pa.maxb = ctx->maxb;
+      pa.dp1 = ctx->dp1;
       pa.rev = next_order(ctx);
       ProfScope ps(ctx, s == 1 ? "pres_1" : "pres_2", 1);
       ctx->nblk[base + 3] = launch_pres(ctx->g, s, pa, ctx->st);
@@ -1170,6 +1174,13 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   cudaMemset(ctx->part, 0, (size_t)NSLOT * 2 * mb * sizeof(double));
   if (cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) { yy_destroy(ctx); return YY_ENOMEM; }
   if ((s = dalloc(ctx, &ctx->ctl, 4)) != YY_OK) { yy_destroy(ctx); return s; }
+  // both patches in this context (the interpolation kernels write every fringe):
+  // system 2 reads p1^(k) - p1^n from one array (YY_DP1=0: off)
+  const char* edp = std::getenv("YY_DP1");
+  if (npatch == 2 && nslab == 1 && !(edp && edp[0] == '0')) {
+    if ((s = dalloc(ctx, &ctx->dp1, npatch * psize(g, KC))) != YY_OK) { yy_destroy(ctx); return s; }
+    cudaMemset(ctx->dp1, 0, npatch * psize(g, KC) * sizeof(double));
+  }
   for (int L = 0; L < 3; ++L)
     for (int f = 0; f < NW; ++f)
       if ((s = dalloc(ctx, &ctx->wl[L][f], 2 * npatch * wsize(g, WKIND[f]))) != YY_OK) { yy_destroy(ctx); return s; }

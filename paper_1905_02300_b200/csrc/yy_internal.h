@@ -46,6 +46,7 @@ struct ResidArgs {
   const double *urit, *urn;  // this system's u_r (iterate, level n)
   const double *utit, *utn;
   const double *p1it, *p1n;
+  const double* dp1;         // p1^(k) - p1^n (both patches, fringe incl.) or NULL: from p1it, p1n
   int rev;                   // reverse block order (bidx)
 };
 
@@ -79,6 +80,7 @@ struct PresArgs {
   double* pit;               // this system's p iterate (updated in place)
   double* part;
   int maxb;
+  double* dp1;               // system 1 writes p1^(k) - p1^n at the solved cells, system 2 reads it (or NULL)
   int rev;                   // reverse block order (bidx)
 };
 
@@ -117,6 +119,8 @@ struct InterpArgs {
   double* up[2];
   CCTab tab_cc;
   VecTab tab_th, tab_ph;
+  double* dp1;               // with p1n: also write p1^(k) - p1^n at the p1 fringe (or NULL)
+  const double* p1n;
 };
 
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);

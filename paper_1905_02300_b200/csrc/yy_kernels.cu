@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
     const double *uti = a.utit + ot, *utn = a.utn + ot;
     const double *upi = a.upit + op, *upn = a.upn + op;
     const double s0 = __ldg(g.sf + j), s1 = __ldg(g.sf + j + 1), sn = __ldg(g.sc + j), is = __ldg(g.is_c + j);
-    auto node = [&](int i) {
+    // the new pressure at cell (i, j, k) (loads only)
+    auto update = [&](int i, long long& q, double& pn) {
       const double ir = __ldg(g.ir_c + i);
       const double f0 = __ldg(g.rf2 + i), f1 = __ldg(g.rf2 + i + 1);
       const double ur0 = 0.5 * (__ldg(uri + IX<KR>(g, i, j, k)) + __ldg(urn + IX<KR>(g, i, j, k)));
@@ -202,26 +203,45 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
       const double up1 = 0.5 * (__ldg(upi + IX<KP>(g, i, j, k + 1)) + __ldg(upn + IX<KP>(g, i, j, k + 1)));
       const double dv = (f1 * ur1 - f0 * ur0) * __ldg(g.idv1_c + i) + (s1 * ut1 - s0 * ut0) * (ir * is * g.idth) +
                         (up1 - up0) * (ir * is * g.idph);
-      const long long q = pc + IX<KC>(g, i, j, k);
-      double nv;
-      if (S == 1) nv = __ldg(a.pn + q) - g.inv_chi * dv;
-      else nv = __ldg(a.pn + q) + (__ldg(a.p1it + q) - __ldg(a.p1n + q)) - g.inv_chi * dv;
-      const double d = nv - a.pit[q];
-      a.pit[q] = nv;
-      w += omega(g, __ldg(g.rc + i), sn) * d * d;
+      q = pc + IX<KC>(g, i, j, k);
+      pn = __ldg(a.pn + q);
+      if (S == 1) return pn - g.inv_chi * dv;
+      return pn + (a.dp1 ? __ldg(a.dp1 + q) : __ldg(a.p1it + q) - __ldg(a.p1n + q)) - g.inv_chi * dv;
     };
-    // 4 r-nodes per thread; system 1 unrolled (all loads of the four nodes in
-    // flight before the first update), system 2 (more arrays per node, already
-    // enough loads in flight) rolled at 32 registers — measured on B200 (C3)
+    // 4 r-nodes per thread.  System 1: the four nodes' loads first (all in flight
+    // together), then the stores (p1, p1^(k) - p1^n); system 2 (more arrays per
+    // node, enough loads in flight already) node by node at 32 registers —
+    // measured on B200 (C3)
     if constexpr (S == 1) {
+      double dv1[4];
+      long long qv[4];
+      int nu = 0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (i0 + u > g.ihi_c) break;
-        node(i0 + u);
+        double pn;
+        const double nv = update(i0 + u, qv[u], pn);
+        const double d = nv - a.pit[qv[u]];
+        a.pit[qv[u]] = nv;
+        w += omega(g, __ldg(g.rc + i0 + u), sn) * d * d;
+        dv1[u] = nv - pn;
+        nu = u + 1;
+      }
+      if (a.dp1) {   // p1^(k) - p1^n for system 2
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nu) a.dp1[qv[u]] = dv1[u];
       }
     } else {
 #pragma unroll 1
-      for (int i = i0; i < i0 + 4 && i <= g.ihi_c; ++i) node(i);
+      for (int i = i0; i < i0 + 4 && i <= g.ihi_c; ++i) {
+        long long q;
+        double pn;
+        const double nv = update(i, q, pn);
+        const double d = nv - a.pit[q];
+        a.pit[q] = nv;
+        w += omega(g, __ldg(g.rc + i), sn) * d * d;
+      }
     }
   }
   const double t = block_sum<128>(w);
@@ -332,6 +352,12 @@ __global__ void k_interp_cc(Geo g, InterpArgs a) {
 #pragma unroll
   for (int u = 0; u < IL; ++u)
     if (i0 + u <= i1) tgt[(long long)(i0 + u) * sr] = v[u];
+  if (q == 1 && a.dp1) {   // p1 fringe: also p1^(k) - p1^n (read by the system-2 residuals)
+    const long long o = patch * ps + (a.tab_cc.tj[e] * NP + a.tab_cc.tk[e]);
+#pragma unroll
+    for (int u = 0; u < IL; ++u)
+      if (i0 + u <= i1) a.dp1[o + (long long)(i0 + u) * sr] = v[u] - __ldg(a.p1n + o + (long long)(i0 + u) * sr);
+  }
 }
 
 // tangential vector components: target kind KT (u_th) or KP (u_ph) of both

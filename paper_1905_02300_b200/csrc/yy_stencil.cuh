@@ -163,9 +163,10 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     // -1/2 grad(p1^(k) - p1^n)   (RD18)
     const int c0 = IX<KC>(g, i, j, k);
     const double *pi_ = a.p1it + pc + c0, *pn = a.p1n + pc + c0;
-    auto dp = [&](int ii, int jj, int kk) {
+    const double* d1 = a.dp1 ? a.dp1 + pc + c0 : nullptr;
+    auto dp = [&](int ii, int jj, int kk) {     // p1^(k) - p1^n (stored once by k_pres<1>, or formed here)
       const int q = (ii - i) * SR<KC>(g) + (jj - j) * ST<KC>(g) + (kk - k);
-      return __ldg(pi_ + q) - __ldg(pn + q);
+      return d1 ? __ldg(d1 + q) : __ldg(pi_ + q) - __ldg(pn + q);
     };
     if (Q == QUR) E -= 0.5 * (dp(i, j, k) - dp(i - 1, j, k)) * g.idr;
     if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) * (__ldg(g.ir_c + i) * g.idth);

@@ -196,17 +196,20 @@ def test_line_solve_every_chunking(shape):
         assert np.array_equal(x2.cpu().numpy(), got), (shape, axis)
 
 
-def test_block_order_alternation_is_bitwise_neutral():
-    """Consecutive residual / sweep / pressure kernels run their blocks in
-    alternating linear order (L2 reuse, YY_ALT_ORDER): every block computes the
-    same tile and the norm partials keep their slots, so the step is bit-identical
-    with the alternation off."""
+@pytest.mark.parametrize("var", ["YY_ALT_ORDER", "YY_DP1"])
+def test_data_path_options_are_bitwise_neutral(var):
+    """YY_ALT_ORDER: consecutive residual / sweep / pressure kernels run their
+    blocks in alternating linear order (L2 reuse) — every block computes the same
+    tile and the norm partials keep their slots.  YY_DP1: system 2 reads
+    p1^(k) - p1^n from one array written by the system-1 pressure update and the
+    p1 fringe interpolation instead of forming it from p1^(k) and p1^n — the same
+    subtraction.  Either way the step is bit-identical with the option off."""
     import os
     cfg = W.small("C3", 9, 17, 47)
     wl = W.random_state(cfg, seed=3, amp=1.0)
     out = []
-    for alt in ("1", "0"):
-        os.environ["YY_ALT_ORDER"] = alt
+    for val in ("1", "0"):
+        os.environ[var] = val
         try:
             sh = _shell(cfg)
             sh.load_workload(wl)
@@ -214,7 +217,7 @@ def test_block_order_alternation_is_bitwise_neutral():
             out.append(([sh.get_fields(p, 0, s) for p in range(2) for s in (1, 2)], sh.stats()))
             sh.close()
         finally:
-            os.environ.pop("YY_ALT_ORDER", None)
+            os.environ.pop(var, None)
     (fa, sa), (fb, sb) = out
     assert sa == sb
     for a, b in zip(fa, fb):
