@@ -128,6 +128,9 @@ __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // axes (bit AX) whose build phase stages its inputs with cp.async; measured on
 // B200 (C3): faster for the phi tiles (one warp per line), slower for r / theta
+#ifndef YY_PSI_EARLY
+#define YY_PSI_EARLY 1
+#endif
 #ifndef YY_LINE_STAGE
 #define YY_LINE_STAGE 4
 #endif
@@ -480,6 +483,18 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       RH[s] = rh * mk;
     }
   }
+  // r/theta final sweeps (YY_PSI_EARLY): psi of the tile is loaded into registers
+  // before the solve, so its DRAM latency overlaps the solve
+  double pv[M];
+  constexpr bool PSE = FINAL && AX != 2 && YY_PSI_EARLY;
+  if (PSE) {
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      int l, e, i, j, k;
+      elem(u, l, e);
+      pv[u] = a.psi[po + node(l, min(e, n - 1), i, j, k)];
+    }
+  }
   __syncthreads();
   // 2.-3. solve chunk c of line l
   {
@@ -558,7 +573,6 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     line_of(t);
   }
   double wsum = 0.0;
-  double pv[M];
   if constexpr (AX == 2 && MODE != MODE_SLAB) {
     // phi: line base pointers, 32-bit row offsets, predicated (not clamped) rows
     double* __restrict__ Pw = a.psi + po + lnd;
@@ -588,7 +602,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       }
     }
   } else {
-  if (FINAL) {
+  if (FINAL && !PSE) {
 #pragma unroll
     for (int u = 0; u < M; ++u) {
       int l, e, i, j, k;
