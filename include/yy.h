@@ -70,6 +70,8 @@ enum {
   YY_HEAT_ONLY = 6,    /* !=0: the heat Douglas scheme eq:HeatDouglas alone: only
                           T is solved (u, p stay as set, normally 0 so a* = 0), the
                           momentum and pressure kernels are skipped, rho_k is T's norm      */
+  YY_INTERP_ORDER = 8, /* fringe interpolation order: 4 (4x4 Lagrange in (theta, phi), RD4) is the
+                          only one built; any other value is YY_EINVAL                       */
   YY_FLUX_FIX = 7      /* eps > 0: Algorithm 1 step 4 every
                           iteration after the fringe exchange — if |net boundary flux| >= tol
                           the fringe normal velocities become the minimiser of J with penalty
@@ -139,6 +141,16 @@ yy_status yy_set_source(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_
                         const yy_fields* terms);
 
 yy_status yy_set_param(yy_ctx* ctx, int32_t key, double value);
+
+/* Device-memory hook (e.g. PyTorch's caching allocator): contexts created after
+ * yy_set_allocator(NULL, alloc, free_, user) obtain every device buffer as
+ * alloc(bytes, user) and return it with free_(ptr, user) at yy_destroy (after a
+ * stream synchronize); alloc = free_ = NULL restores cudaMalloc / cudaFree.
+ * A context allocates everything at yy_create, so ctx != NULL is YY_ESTATE.
+ * alloc returning NULL fails the create with YY_ENOMEM.  Not thread-safe
+ * against concurrent yy_create calls. */
+yy_status yy_set_allocator(yy_ctx* ctx, void* (*alloc)(size_t bytes, void* user), void (*free_)(void* ptr, void* user),
+                           void* user);
 
 /* Launch every kernel on this stream (a cudaStream_t, e.g.
  * torch.cuda.current_stream().cuda_stream).  Default: the legacy stream. */

@@ -110,6 +110,10 @@ struct yy_ctx {
   int stf[2][MAXSRC] = {};
   // interpolation tables (device)
   std::vector<void*> allocs;
+  // device memory hook (yy_set_allocator; copied from the process default at create)
+  void* (*alloc_fn)(size_t, void*) = nullptr;
+  void (*free_fn)(void*, void*) = nullptr;
+  void* alloc_user = nullptr;
   CCTab tcc{};
   VecTab tth{}, tph{};
   std::vector<int> st_iters;
@@ -141,8 +145,14 @@ yy_status fail(yy_ctx* c, yy_status s, const std::string& msg) {
 template <class T>
 yy_status dalloc(yy_ctx* ctx, T** p, size_t count) {
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
-  if (e != cudaSuccess) return fail(ctx, YY_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  const size_t bytes = count * sizeof(T) + 16;
+  if (ctx->alloc_fn) {                       // injected allocator (yy_set_allocator)
+    q = ctx->alloc_fn(bytes, ctx->alloc_user);
+    if (!q) return fail(ctx, YY_ENOMEM, "injected allocator returned NULL");
+  } else {
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) return fail(ctx, YY_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
   ctx->allocs.push_back(q);
   *p = static_cast<T*>(q);
   return YY_OK;
@@ -1015,6 +1025,13 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
 namespace {
 // npatch local patches starting at global patch0; nslab > 1: radial slab `slab`
 // of nslab equal slabs (nr / nslab rows, plus one halo row on each side)
+// process-wide allocator for contexts created from now on (yy_set_allocator(NULL, ...))
+struct AllocHook {
+  void* (*alloc)(size_t, void*) = nullptr;
+  void (*free_)(void*, void*) = nullptr;
+  void* user = nullptr;
+} g_alloc;
+
 yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double Ra, double dt, int npatch,
                      int patch0, yy_ctx** out, int nslab = 1, int slab = 0) {
   if (!out) return YY_EINVAL;
@@ -1029,6 +1046,9 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if ((double)(gr->nr + 1) * (gr->ntheta + 1) * (gr->nphi + 1) >= 2147483647.0) return YY_EINVAL;
   if (!(R1 > 0 && R2 > R1) || !(dt > 0) || !(Pr > 0) || !std::isfinite(Ra)) return YY_EINVAL;
   yy_ctx* ctx = new yy_ctx();
+  ctx->alloc_fn = g_alloc.alloc;
+  ctx->free_fn = g_alloc.free_;
+  ctx->alloc_user = g_alloc.user;
   if (const char* e = std::getenv("YY_FUSE")) ctx->fuse = (e[0] && e[0] != '0');
   if (const char* e = std::getenv("YY_ALT_ORDER")) ctx->alt_order = !(e[0] == '0');
   if (const char* e = std::getenv("YY_GRAPH")) ctx->use_graph = (e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
@@ -1417,6 +1437,9 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       if (ctx->mode == 1)
         for (yy_ctx* c : ctx->group) if (c) c->heat_only = ctx->heat_only;
       return YY_OK;
+    case YY_INTERP_ORDER:
+      if (v != 4) return fail(ctx, YY_EINVAL, "interpolation order: only 4 (4x4 Lagrange, RD4) is built");
+      return YY_OK;
     case YY_PROFILE:
       cudaStreamSynchronize(ctx->st);
       prof_collect(ctx);
@@ -1425,6 +1448,15 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       return YY_OK;
   }
   return fail(ctx, YY_EINVAL, "unknown parameter key");
+}
+
+yy_status yy_set_allocator(yy_ctx* ctx, void* (*alloc)(size_t, void*), void (*free_)(void*, void*), void* user) {
+  if ((alloc == nullptr) != (free_ == nullptr)) return ctx ? fail(ctx, YY_EINVAL, "alloc and free go together") : YY_EINVAL;
+  if (ctx) return fail(ctx, YY_ESTATE, "a context allocates at yy_create: set the allocator with ctx = NULL first");
+  g_alloc.alloc = alloc;
+  g_alloc.free_ = free_;
+  g_alloc.user = user;
+  return YY_OK;
 }
 
 yy_status yy_set_stream(yy_ctx* ctx, void* stream) {
@@ -1505,7 +1537,11 @@ void yy_destroy(yy_ctx* ctx) {
       if (c && c != ctx)
         for (auto& m : c->group) if (m == ctx) m = nullptr;
   if (ctx->mode == 2 && ctx->nccl) nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->nccl));
-  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->alloc_fn) cudaStreamSynchronize(ctx->st);   // (a caching allocator may hand the memory on)
+  for (void* p : ctx->allocs) {
+    if (ctx->alloc_fn) ctx->free_fn(p, ctx->alloc_user);
+    else cudaFree(p);
+  }
   if (ctx->red_host) cudaFreeHost(ctx->red_host);
   delete ctx;
 }

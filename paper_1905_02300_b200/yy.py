@@ -16,12 +16,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 YY_OK, YY_ENOCONV = 0, 4
 YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ, YY_HEAT_ONLY, YY_FLUX_FIX = 1, 2, 3, 4, 5, 6, 7
+YY_INTERP_ORDER = 8
 TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
            "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_time",
            "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve", "yy_line_prepare", "yy_launch_count",
-           "yy_profile_report")
+           "yy_profile_report", "yy_set_allocator")
 
 
 class YYError(RuntimeError):
@@ -37,6 +38,10 @@ _DP = POINTER(c_double)
 
 class yy_fields(ctypes.Structure):
     _fields_ = [("ur", _DP), ("ut", _DP), ("up", _DP), ("p", _DP), ("T", _DP)]
+
+
+ALLOC_FN = ctypes.CFUNCTYPE(c_void_p, ctypes.c_size_t, c_void_p)   # yy_set_allocator callbacks
+FREE_FN = ctypes.CFUNCTYPE(None, c_void_p, c_void_p)
 
 
 def lib_path() -> str:
@@ -75,6 +80,8 @@ def load_library():
     L.yy_debug_get.argtypes = [ctx, c_char_p, c_int32, _DP]
     L.yy_line_solve.argtypes = [ctx, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
     L.yy_line_prepare.argtypes = [ctx, c_void_p, c_void_p, c_void_p]
+    L.yy_set_allocator.argtypes = [ctx, ALLOC_FN, FREE_FN, c_void_p]
+    L.yy_set_allocator.restype = c_int32
     L.yy_launch_count.argtypes = [ctx]
     L.yy_launch_count.restype = ctypes.c_int64
     L.yy_profile_report.argtypes = [ctx, ctypes.c_char_p, c_int32]
@@ -86,7 +93,7 @@ def load_library():
     L.yy_nccl_unique_id.argtypes = [c_void_p]
     for name in ("yy_create_pair", "yy_create_slabs", "yy_create_dist", "yy_nccl_unique_id", "yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
                  "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve", "yy_line_prepare",
-                 "yy_profile_report"):
+                 "yy_profile_report", "yy_set_allocator"):
         getattr(L, name).restype = c_int32
     _lib = L
     return L
@@ -338,3 +345,37 @@ def nccl_unique_id():
     if st != YY_OK:
         raise YYError(f"yy_nccl_unique_id failed with status {st} (NCCL not loadable?)")
     return buf.raw
+
+
+_alloc_keep = []   # every callback pair ever installed: contexts created with it free through it
+
+
+def use_torch_allocator(enable: bool = True, device=None):
+    """Route the device buffers of every context created from now on through
+    PyTorch's caching allocator (yy_set_allocator(NULL, ...)); enable=False
+    restores cudaMalloc for later contexts.  The callbacks stay alive for the
+    life of the process (a context frees through the pair it was created with)."""
+    L = load_library()
+    if not enable:
+        st = L.yy_set_allocator(None, ALLOC_FN(), FREE_FN(), None)
+    else:
+        import torch
+        dev = torch.cuda.current_device() if device is None else device
+
+        def alloc(nbytes, user):
+            try:
+                return torch.cuda.caching_allocator_alloc(nbytes, dev)
+            except Exception:   # -> NULL -> YY_ENOMEM
+                return None
+
+        def free(ptr, user):
+            try:
+                torch.cuda.caching_allocator_delete(ptr)
+            except Exception:   # interpreter shutdown: torch already gone
+                pass
+
+        keep = (ALLOC_FN(alloc), FREE_FN(free))
+        _alloc_keep.append(keep)
+        st = L.yy_set_allocator(None, keep[0], keep[1], None)
+    if st != YY_OK:
+        raise YYError(f"yy_set_allocator failed with status {st}")

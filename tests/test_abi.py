@@ -44,3 +44,14 @@ def test_binding_refuses_without_library(tmp_path, monkeypatch):
     except yy.YYError:
         return
     raise AssertionError("binding must fail loudly when libyy.so is missing")
+
+
+def test_allocator_hook_host_logic():
+    """yy_set_allocator: process default only (ctx = NULL), alloc / free in pairs."""
+    import paper_1905_02300_b200 as pkg
+    from paper_1905_02300_b200.yy import ALLOC_FN, FREE_FN
+    L = pkg.load_library()
+    assert L.yy_set_allocator(None, ALLOC_FN(), FREE_FN(), None) == 0            # reset: cudaMalloc
+    half = ALLOC_FN(lambda n, u: 0)
+    assert L.yy_set_allocator(None, half, FREE_FN(), None) == -2                 # YY_EINVAL
+    assert L.yy_set_allocator(None, ALLOC_FN(), FREE_FN(), None) == 0

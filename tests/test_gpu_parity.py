@@ -225,6 +225,52 @@ def test_data_path_options_are_bitwise_neutral(var):
             assert np.array_equal(a[k], b[k]), k
 
 
+def test_torch_caching_allocator_hook():
+    """yy_set_allocator through PyTorch's caching allocator: the context's buffers
+    come from torch (memory_allocated grows by at least the state's size and
+    returns at destroy) and the step is bit-identical to cudaMalloc buffers."""
+    import torch
+    from paper_1905_02300_b200 import use_torch_allocator
+    cfg = W.small("C3", 8, 16, 40)
+    wl = W.make_workload(cfg)
+    out = []
+    for hook in (True, False):
+        use_torch_allocator(hook)
+        try:
+            torch.cuda.synchronize()
+            m0 = torch.cuda.memory_allocated()
+            sh = _shell(cfg)
+            torch.cuda.synchronize()
+            m1 = torch.cuda.memory_allocated()
+            if hook:
+                # at least the 32 (nr, nth, nph) state arrays of both patches
+                assert m1 - m0 >= 32 * 2 * cfg.nr * cfg.nth * cfg.nph * 8, (m0, m1)
+            else:
+                assert m1 == m0
+            sh.load_workload(wl)
+            sh.step(2, cfg.tol)
+            out.append(([sh.get_fields(p, 0, s) for p in range(2) for s in (1, 2)], sh.stats()))
+            sh.close()
+            torch.cuda.synchronize()
+            assert torch.cuda.memory_allocated() == m0
+        finally:
+            use_torch_allocator(False)
+    (fa, sa), (fb, sb) = out
+    assert sa == sb
+    for a, b in zip(fa, fb):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+
+
+def test_interp_order_param():
+    from paper_1905_02300_b200 import YYError
+    from paper_1905_02300_b200.yy import YY_INTERP_ORDER
+    sh = _shell(W.small("C1", 4, 12, 28))
+    sh.set_param(YY_INTERP_ORDER, 4)
+    with pytest.raises(YYError):
+        sh.set_param(YY_INTERP_ORDER, 2)
+
+
 def test_errors_are_reported():
     from paper_1905_02300_b200 import YYError
     cfg = W.small("C1", 4, 12, 28)
