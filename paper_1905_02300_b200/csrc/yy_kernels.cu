@@ -590,18 +590,21 @@ void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   const dim3 grid((NPk(g, K) - 2 + BK - 1) / BK, (NTk(g, K) - 2 + BJ - 1) / BJ, g.npatch * nch);
   k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
 }
-// r-nodes per thread of the residual, per quantity (measured on B200, C3);
-// YY_RESID_IB=<T>,<ur>,<ut>,<up> overrides (tuning)
+// r-nodes per thread of the residual per (quantity, system), measured on B200
+// (C3): T 2, u_r 2 / 1, u_th 2 / 2, u_ph 4 / 4.  YY_RESID_IB=<T>,<ur1>,<ur2>,<ut1>,
+// <ut2>,<up1>,<up2> overrides (tuning)
 template <int Q, int S>
 void resid_q(const Geo& g, const ResidArgs& a, cudaStream_t st) {
-  static int ib[4] = {-1, -1, -1, -1};
+  static int ib[7] = {-1, -1, -1, -1, -1, -1, -1};
   if (ib[0] < 0) {
-    const int def[4] = {2, 2, 2, 2};
-    for (int q = 0; q < 4; ++q) ib[q] = def[q];
-    if (const char* e = getenv("YY_RESID_IB")) sscanf(e, "%d,%d,%d,%d", &ib[0], &ib[1], &ib[2], &ib[3]);
+    const int def[7] = {2, 2, 1, 2, 2, 4, 4};
+    for (int q = 0; q < 7; ++q) ib[q] = def[q];
+    if (const char* e = getenv("YY_RESID_IB"))
+      sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &ib[0], &ib[1], &ib[2], &ib[3], &ib[4], &ib[5], &ib[6]);
   }
-  if (ib[Q] == 1) resid_qb<Q, S, 1>(g, a, st);
-  else if (ib[Q] == 2) resid_qb<Q, S, 2>(g, a, st);
+  const int b = ib[Q == QT ? 0 : 2 * Q - 2 + S];
+  if (b == 1) resid_qb<Q, S, 1>(g, a, st);
+  else if (b == 2) resid_qb<Q, S, 2>(g, a, st);
   else resid_qb<Q, S, 4>(g, a, st);
 }
 
