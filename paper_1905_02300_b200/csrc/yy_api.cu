@@ -76,8 +76,9 @@ struct yy_ctx {
   double* fr_recv = nullptr;   // fringe values received for this patch
   long long fr_n = 0;
   // radial slabs: partitioned r-sweep buffers and the gathered norm sums
-  double* V = nullptr;
-  double* W = nullptr;
+  double* Vq[4] = {};          // per quantity: the r-lines' responses to the lower / upper
+  double* Wq[4] = {};          // neighbour slab's boundary unknown (per step)
+  bool vw_fresh = true;        // this iteration writes Vq / Wq (the step's first)
   double* IF = nullptr;        // [nlines][6] this slab's boundary rows
   double* IFall = nullptr;     // [nslab][nlines][6] every slab of the patch
   double* LH = nullptr;        // [nlines][2]
@@ -613,7 +614,10 @@ SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
   w.R = ctx->R; w.psi = ctx->it[qfield(q, s)];
   w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
   w.maxb = ctx->maxb;
-  w.V = ctx->V; w.W = ctx->W; w.IF = ctx->IF;
+  // radial slabs: V, W of quantity q's r-factor (one matrix per step, shared by
+  // both systems) are written by the first iteration of the step only
+  w.V = ctx->Vq[q]; w.W = ctx->Wq[q]; w.IF = ctx->IF;
+  w.vw = ctx->vw_fresh && (q == QT || s == 1);
   return w;
 }
 
@@ -973,6 +977,7 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   }
   while (k < kmax) {
     ++k;
+    for (yy_ctx* c : cs) c->vw_fresh = (k == 1);   // slab V / W: once per step (the step's matrices)
     if (graph) {
       const cudaError_t el = cudaGraphLaunch(gexec, ctx->st);
       if (el != cudaSuccess) { cudaGraphExecDestroy(gexec); CK(el); }
@@ -1214,7 +1219,12 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if (nslab > 1) {     // partitioned r-sweep buffers
     long long nlmax = 0;
     for (int K = 0; K < 4; ++K) nlmax = std::max(nlmax, (long long)(NTk(g, K) - 2) * (NPk(g, K) - 2));
-    if ((s = dalloc(ctx, &ctx->V, maxk)) != YY_OK || (s = dalloc(ctx, &ctx->W, maxk)) != YY_OK ||
+    for (int q = 0; q < 4; ++q)
+      if ((s = dalloc(ctx, &ctx->Vq[q], psize(g, q))) != YY_OK || (s = dalloc(ctx, &ctx->Wq[q], psize(g, q))) != YY_OK) {
+        yy_destroy(ctx);
+        return s;
+      }
+    if (
         (s = dalloc(ctx, &ctx->IF, 6 * nlmax)) != YY_OK || (s = dalloc(ctx, &ctx->IFall, 6 * nslab * nlmax)) != YY_OK ||
         (s = dalloc(ctx, &ctx->LH, 2 * nlmax)) != YY_OK) { yy_destroy(ctx); return s; }
   }

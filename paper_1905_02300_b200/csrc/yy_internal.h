@@ -63,6 +63,8 @@ struct SweepArgs {
   double* V;
   double* W;
   double* IF;                // [line][6], line = (j-1)(np_k-2) + (k-1)
+  int vw;                    // write V, W (they depend on the step's matrix only: the first
+                             // iteration of a step writes them, later ones reuse them)
   int rev;                   // run the grid's blocks in reverse linear order (bidx)
 };
 

@@ -624,8 +624,10 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       } else if (MODE == MODE_SLAB) {
         const double xl = LO[slot(l, e)], xh = UP[slot(l, e)];
         R[nd] = x;
-        a.V[po + nd] = xl;
-        a.W[po + nd] = xh;
+        if (a.vw) {                           // (per-step: the line's responses to its couplings)
+          a.V[po + nd] = xl;
+          a.W[po + nd] = xh;
+        }
         if (e == 0 || e == n - 1) {           // this slab's boundary rows of the line
           double* f = a.IF + 6LL * ((j - 1) * (NPk(g, K) - 2) + (k - 1)) + (e == 0 ? 0 : 3);
           f[0] = x;
