@@ -6,24 +6,31 @@
 //
 // One design for the three axes: a line of n rows is split into P contiguous
 // chunks of M rows (P*M >= n; rows past n are identity rows), one chunk per
-// thread, the P threads of a line forming an aligned segment of a warp.  Every
-// thread keeps its chunk in REGISTERS and
-//   1. builds its rows (normalised by the diagonal) from b and the transport
-//      velocity a*  (coef<> of yy_dev.cuh, the rows the residual applies);
-//   2. eliminates the chunk interior with the chunk's last unknown g_c and the
-//      previous chunk's g_{c-1} kept symbolic: x_t = y_t + v_t g_{c-1} + w_t g_c
-//      (one reciprocal per row) — the Schur-complement partition of the
-//      distributed tridiagonal solve of P:L477-480, here across warp lanes;
-//   3. solves the P-unknown interface system by log2(P) steps of parallel
-//      cyclic reduction over segment shuffles;
-//   4. back-fills x and writes it (or psi += x and the convergence norm, FINAL).
-// No shared-memory round trips and no c'/d' scratch in HBM: an r or theta line
-// costs exactly its algorithmic bytes (read b, read a*, write x).
+// thread, the P threads of a line forming an aligned segment of a warp.  A block
+// (128 threads) owns 128/P lines:
+//   1. build: every row of the tile (normalised by its diagonal) from b and the
+//      per-step row weights (coef_split / coef of yy_dev.cuh, the rows the
+//      residual applies), written coalesced into a chunk-major shared-memory
+//      tile (odd line pitch);
+//   2. each thread loads its chunk into REGISTERS and eliminates the chunk
+//      interior with the chunk's last unknown g_c and the previous chunk's
+//      g_{c-1} kept symbolic: x_t = y_t + v_t g_{c-1} + w_t g_c (one reciprocal
+//      per row) — the Schur-complement partition of the distributed tridiagonal
+//      solve of P:L477-480, here across warp lanes;
+//   3. the P-unknown interface system by log2(P) steps of parallel cyclic
+//      reduction over segment shuffles (select-free);
+//   4. back-fill, x back to the tile, then written coalesced (or psi += x and the
+//      convergence norm partial, FINAL).
+// No c'/d' scratch in HBM: a sweep moves its algorithmic bytes (read b and the
+// row weight, write x; FINAL also psi).
 //
-// r and theta lines (strided): a warp covers 32/P consecutive phi-lines, so a
-// load of row t touches P segments of 256/P contiguous bytes (full sectors).
-// phi lines (contiguous): the rows are built coalesced into shared memory in
-// chunk-major layout (odd pitch, conflict-free), then read back per chunk.
+// r and theta lines (strided): consecutive threads take consecutive phi-lines
+// (128/P per block) in the build, each walking rows of its chunk; the loads of b
+// are batched in registers, the row weights L1-prefetched first.
+// phi lines (contiguous): one warp (P = 32 threads) per line, the tile's b, row
+// weights and reaction values staged in shared memory with cp.async; lines
+// longer than 384 rows take four warps (segments with symbolic couplings, then
+// the line's 8-unknown boundary system, as for radial slabs).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
