@@ -897,10 +897,13 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   // (a*, G and the level pointers are fixed for the step): capture it once per
   // step as a CUDA graph (single context on a user stream, not profiling) and
   // replay it — the ~35 kernels then follow each other without per-launch gaps.
-  const bool graph = ctx->use_graph && cs.size() == 1 && ctx->mode == 0 && ctx->st != nullptr && !ctx->prof_on;
+  // graphs: one context (mode 0) or a loopback group on one shared stream
+  // (mode 1, additive Schwarz); NCCL ranks (mode 2) launch stream by stream
+  const bool graph = ctx->use_graph && ctx->st != nullptr && !ctx->prof_on &&
+                     ((cs.size() == 1 && ctx->mode == 0) || (ctx->mode == 1 && ctx->schwarz == 0));
   cudaGraphExec_t gexec = nullptr;
-  long long glaunches = 0;
-  if (graph && ctx->use_graph == 2) {
+  std::vector<long long> glaunches(cs.size(), 0);
+  if (graph && ctx->use_graph == 2 && cs.size() == 1 && ctx->mode == 0) {
     // the whole loop on the device: a WHILE node whose body is one iteration
     // (O5-O10) followed by k_schwarz_cond; one launch and one host sync per step
     const long long l0 = ctx->launches;
@@ -958,7 +961,11 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   }
   if (graph) {
     cudaGraph_t gr = nullptr;
-    const long long l0 = ctx->launches;
+    std::vector<long long> l0(cs.size());
+    for (size_t q = 0; q < cs.size(); ++q) {
+      l0[q] = cs[q]->launches;
+      cs[q]->vw_fresh = true;      // (the replayed iteration also writes the slab V / W)
+    }
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     yy_status sc = exchange_fringe(cs);
     if (sc == YY_OK) { flux_fix(cs, tol); sc = iter_solve(cs); }
@@ -972,16 +979,19 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     const cudaError_t ei = cudaGraphInstantiate(&gexec, gr, 0);
     cudaGraphDestroy(gr);
     CK(ei);
-    glaunches = ctx->launches - l0;
-    ctx->launches = l0;
+    for (size_t q = 0; q < cs.size(); ++q) {
+      glaunches[q] = cs[q]->launches - l0[q];
+      cs[q]->launches = l0[q];
+    }
   }
   while (k < kmax) {
     ++k;
-    for (yy_ctx* c : cs) c->vw_fresh = (k == 1);   // slab V / W: once per step (the step's matrices)
+    if (!graph)
+      for (yy_ctx* c : cs) c->vw_fresh = (k == 1);   // slab V / W: once per step (the step's matrices)
     if (graph) {
       const cudaError_t el = cudaGraphLaunch(gexec, ctx->st);
       if (el != cudaSuccess) { cudaGraphExecDestroy(gexec); CK(el); }
-      ctx->launches += glaunches;
+      for (size_t q = 0; q < cs.size(); ++q) cs[q]->launches += glaunches[q];
     } else if (ctx->schwarz == 1) {                        // multiplicative: Yin, then Yang with Yin's k
       for (int p = 0; p < 2; ++p) {
         TRY(exchange_fringe_to(cs, p));                    // O5 for patch p

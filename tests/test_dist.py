@@ -261,3 +261,45 @@ def test_flux_fix_matches_oracle(layout):
                 assert np.max(np.abs(b[k] - c[k])) / den <= 1e-11, (p, s, k)
                 moved = max(moved, np.max(np.abs(c[k] - d[k])) / den)
     assert moved > 1e-9          # the correction changed the iterates
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nslab", [1, 2])
+def test_loopback_group_graph_is_bitwise_the_stream_path(nslab):
+    """A loopback group on a user stream replays each Schwarz iteration as one
+    CUDA graph (all members' kernels and transfers, the slab V / W written every
+    replay): bit-identical to the stream launches (YY_GRAPH=0), same counts."""
+    import os
+    import torch
+    from paper_1905_02300_b200 import Shell
+    cfg = W.small("C3", 32, 14, 40)        # slabs of 16 rows (the slab chunk menu)
+    wl = W.make_workload(cfg)
+    args = (cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    out = []
+    for graph in ("1", "0"):
+        os.environ["YY_GRAPH"] = graph
+        try:
+            st = torch.cuda.Stream()
+            grp = (Shell.pair(*args, stream=st.cuda_stream) if nslab == 1
+                   else Shell.slabs(*args, nslab=nslab, stream=st.cuda_stream))
+            for sh in grp:
+                sh.load_workload(wl)
+            grp[0].step(3, cfg.tol)
+            torch.cuda.synchronize()
+            def whole(p, s):      # every member's rows of patch p, assembled
+                names = ("ur", "ut", "up", "p", "T")
+                f = {n: np.zeros(grp[0].shape(n)) for n in names}
+                for sh in grp:
+                    if p in sh.patches:
+                        sh.get_fields(p, 0, s, out=f)
+                return f
+            out.append(([whole(p, s) for p in range(2) for s in (1, 2)], grp[0].stats()))
+            for sh in grp:
+                sh.close()
+        finally:
+            os.environ.pop("YY_GRAPH", None)
+    (fa, sa), (fb, sb) = out
+    assert sa == sb
+    for a, b in zip(fa, fb):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
