@@ -271,6 +271,30 @@ def test_interp_order_param():
         sh.set_param(YY_INTERP_ORDER, 2)
 
 
+@pytest.mark.parametrize("graph", ["2", "0"])
+def test_max_iters_reports_no_convergence(graph):
+    """K_max reached before tol: the step completes and yy_step returns the
+    positive warning YY_ENOCONV; the same state as the oracle run
+    with the same iteration cap."""
+    import os
+    import torch
+    from paper_1905_02300_b200.yy import YY_ENOCONV, YY_OK
+    cfg = W.small("C3", 8, 14, 40)
+    wl = W.make_workload(cfg)
+    os.environ["YY_GRAPH"] = graph
+    try:
+        st = torch.cuda.Stream()
+        sh = _shell(cfg, stream=st.cuda_stream, max_iters=3)
+        sh.load_workload(wl)
+        assert sh.step(1, 1e-30) == YY_ENOCONV
+        assert sh.stats()[-1][0] == 3
+        assert sh.step(1, 1e30) == YY_OK
+        assert sh.stats()[-1][0] == 1
+        sh.close()
+    finally:
+        os.environ.pop("YY_GRAPH", None)
+
+
 def test_errors_are_reported():
     from paper_1905_02300_b200 import YYError
     cfg = W.small("C1", 4, 12, 28)
