@@ -102,6 +102,10 @@ struct yy_ctx {
   double* red_host = nullptr;   // pinned
   double* ctl = nullptr;        // device-side Schwarz loop: iterations, rho, NaN flag
   double* dp1 = nullptr;        // p1^(k) - p1^n, both patches (two-patch contexts; NULL otherwise)
+  // two-patch contexts: the three fringe interpolation classes run concurrently
+  // (fork / join on st; YY_PAR_INTERP=0: one after the other)
+  cudaStream_t aux[2] = {};
+  cudaEvent_t fork[3] = {};
   double* wterm[2][MAXSRC][NW] = {};
   int nw[2] = {0, 0};
   int wtf[2][MAXSRC] = {};
@@ -810,7 +814,8 @@ yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
   if (!distributed(cs)) {
     yy_ctx* ctx = cs[0];
     ProfScope ps(ctx, "interp", 3);
-    launch_interp(ctx->g, interp_args(ctx), ctx->st);
+    if (ctx->aux[0]) launch_interp(ctx->g, interp_args(ctx), ctx->st, ctx->aux[0], ctx->aux[1], ctx->fork);
+    else launch_interp(ctx->g, interp_args(ctx), ctx->st);
     return YY_OK;
   }
   for (yy_ctx* ctx : cs) {                                // donor side: the partner's fringe
@@ -1211,6 +1216,13 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   if ((s = dalloc(ctx, &ctx->ctl, 4)) != YY_OK) { yy_destroy(ctx); return s; }
   // both patches in this context (the interpolation kernels write every fringe):
   // system 2 reads p1^(k) - p1^n from one array (YY_DP1=0: off)
+  const char* epi = std::getenv("YY_PAR_INTERP");
+  if (npatch == 2 && nslab == 1 && !(epi && epi[0] == '0')) {
+    for (int q = 0; q < 2; ++q)
+      if (cudaStreamCreateWithFlags(&ctx->aux[q], cudaStreamNonBlocking) != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
+    for (int q = 0; q < 3; ++q)
+      if (cudaEventCreateWithFlags(&ctx->fork[q], cudaEventDisableTiming) != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }
+  }
   const char* edp = std::getenv("YY_DP1");
   if (npatch == 2 && nslab == 1 && !(edp && edp[0] == '0')) {
     if ((s = dalloc(ctx, &ctx->dp1, npatch * psize(g, KC))) != YY_OK) { yy_destroy(ctx); return s; }
@@ -1563,6 +1575,8 @@ void yy_destroy(yy_ctx* ctx) {
     else cudaFree(p);
   }
   if (ctx->red_host) cudaFreeHost(ctx->red_host);
+  for (cudaStream_t a : ctx->aux) if (a) cudaStreamDestroy(a);
+  for (cudaEvent_t e : ctx->fork) if (e) cudaEventDestroy(e);
   delete ctx;
 }
 

@@ -165,7 +165,10 @@ void launch_reduce_final(double* out, cudaStream_t st);
 // node's condition h (continue: no NaN, k < kmax, fixed or rho >= tol)
 void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double* ctl, double tol, int kmax,
                          bool fixed, cudaStream_t st);
-void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st);
+// the three fringe classes (cell/r-face lattice, theta faces, phi faces); with s2,
+// s3 and ev[3] given they run concurrently (fork / join on st through the events)
+void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st, cudaStream_t s2 = nullptr,
+                   cudaStream_t s3 = nullptr, cudaEvent_t* ev = nullptr);
 // one patch per context: the donor evaluates the partner's fringe values from its
 // own patch into buf (pack), the target writes a received buf into its fringe
 // (unpack).  Layout: [cc: 5 x (nr+1) x n_cc][th: 2 x nr x n_th][ph: 2 x nr x n_ph].

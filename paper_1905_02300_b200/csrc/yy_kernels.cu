@@ -650,11 +650,24 @@ void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double
   k_schwarz_cond<<<1, 32, 0, st>>>(h, red, ctl, tol, kmax, fixed ? 1 : 0);
 }
 
-void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st) {
+void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st, cudaStream_t s2, cudaStream_t s3,
+                   cudaEvent_t* ev) {
   const int ngc = (g.nr + 1 + IL - 1) / IL, ngv = (g.nr + IL - 1) / IL;
+  const bool par = s2 && s3 && ev;
+  if (par) {
+    cudaEventRecord(ev[0], st);
+    cudaStreamWaitEvent(s2, ev[0], 0);
+    cudaStreamWaitEvent(s3, ev[0], 0);
+  }
   if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 10), 128, 0, st>>>(g, a);
-  if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, ngv, 4), 128, 0, st>>>(g, a);
-  if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, ngv, 4), 128, 0, st>>>(g, a);
+  if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, ngv, 4), 128, 0, par ? s2 : st>>>(g, a);
+  if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, ngv, 4), 128, 0, par ? s3 : st>>>(g, a);
+  if (par) {
+    cudaEventRecord(ev[1], s2);
+    cudaEventRecord(ev[2], s3);
+    cudaStreamWaitEvent(st, ev[1], 0);
+    cudaStreamWaitEvent(st, ev[2], 0);
+  }
 }
 
 long long fringe_count(const Geo& g, const InterpArgs& a) {
