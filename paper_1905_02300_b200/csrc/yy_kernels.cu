@@ -294,21 +294,8 @@ __global__ void k_reduce_final(double* __restrict__ out) {
 // K5: Yin<->Yang fringe interpolation (Alg.1 steps 1,3,7; RD3-RD5).
 // Reads donor solved nodes, writes target fringe nodes: race-free in place.
 // ---------------------------------------------------------------------------------
-__device__ __forceinline__ double interp16(const Geo& g, int K, const double* __restrict__ X, int i, int jb,
-                                           int kb, const double* __restrict__ w) {
-  const int NT = NTk(g, K), NP = NPk(g, K);
-  const double* base = X + ((long long)i * NT + jb) * NP + kb;
-  double v = 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const double* row = base + (long long)a * NP;
-    const double s = w[4] * row[0] + w[5] * row[1] + w[6] * row[2] + w[7] * row[3];
-    v += w[a] * s;
-  }
-  return v;
-}
-
-// the same with the 8 weights in registers and read-only donor loads
+// 4x4 Lagrange stencil at base (rows NP apart) with the entry's 8 weights
+// (w[0..3] across rows, w[4..7] along a row) in registers; read-only donor loads
 __device__ __forceinline__ double interp16r(const double* __restrict__ base, int NP, const double (&w)[8]) {
   double v = 0.0;
 #pragma unroll
@@ -401,14 +388,28 @@ __global__ void k_interp_vec(Geo g, InterpArgs a) {
 // partner's fringe with the partner's own entries, from its local patch.
 // grid: x -> entry, y -> i, z -> quantity
 __global__ void k_pack_cc(Geo g, InterpArgs a, double* __restrict__ buf) {
+  // grid y: groups of IL r-levels (the entry's stencil read once, as k_interp_cc)
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y, q = blockIdx.z;
+  const int q = blockIdx.z;
   if (e >= a.tab_cc.n) return;
   const int K = (q < 3) ? KC : KR;
-  if (K == KC && (i < g.ifr_c0 || i > g.ifr_c1)) return;
-  if (K == KR && (i < g.ifr_f0 || i > g.ifr_f1)) return;
-  const int jb = a.tab_cc.jb[e], kb = a.tab_cc.kb[e];
-  buf[((long long)q * (g.nr + 1) + i) * a.tab_cc.n + e] = interp16(g, K, a.cc[q], i, jb, kb, a.tab_cc.w + 8LL * e);
+  const int lo = K == KC ? g.ifr_c0 : g.ifr_f0, hi = K == KC ? g.ifr_c1 : g.ifr_f1;
+  const int i0 = max(lo, (int)blockIdx.y * IL);
+  const int i1 = min(hi, (int)blockIdx.y * IL + IL - 1);
+  if (i0 > i1) return;
+  const int NT = NTk(g, K), NP = NPk(g, K);
+  double w[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) w[m] = __ldg(a.tab_cc.w + 8LL * e + m);
+  const double* donor = a.cc[q] + (a.tab_cc.jb[e] * NP + a.tab_cc.kb[e]);
+  const long long sr = (long long)NT * NP;
+  double v[IL];
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1) v[u] = interp16r(donor + (i0 + u) * sr, NP, w);
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1) buf[((long long)q * (g.nr + 1) + i0 + u) * a.tab_cc.n + e] = v[u];
 }
 __global__ void k_unpack_cc(Geo g, InterpArgs a, const double* __restrict__ buf) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -425,11 +426,29 @@ template <int KTGT>
 __global__ void k_pack_vec(Geo g, InterpArgs a, double* __restrict__ buf) {
   const VecTab& t = (KTGT == KT) ? a.tab_th : a.tab_ph;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y, s = blockIdx.z;
-  if (e >= t.n || i < g.ifr_c0 || i > g.ifr_c1) return;
-  const double vt = interp16(g, KT, a.ut[s], i, t.jb_t[e], t.kb_t[e], t.w_t + 8LL * e);
-  const double vp = interp16(g, KP, a.up[s], i, t.jb_p[e], t.kb_p[e], t.w_p + 8LL * e);
-  buf[((long long)s * g.nr + i) * t.n + e] = t.m0[e] * vt + t.m1[e] * vp;
+  const int s = blockIdx.z;
+  const int i0 = max(g.ifr_c0, (int)blockIdx.y * IL);
+  const int i1 = min(g.ifr_c1, (int)blockIdx.y * IL + IL - 1);
+  if (e >= t.n || i0 > i1) return;
+  const int NPT = NPk(g, KT), NPP = NPk(g, KP);
+  const long long srt = (long long)NTk(g, KT) * NPT, srp = (long long)NTk(g, KP) * NPP;
+  const double* dut = a.ut[s] + (t.jb_t[e] * NPT + t.kb_t[e]);
+  const double* dup = a.up[s] + (t.jb_p[e] * NPP + t.kb_p[e]);
+  double wt[8], wp[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    wt[m] = __ldg(t.w_t + 8LL * e + m);
+    wp[m] = __ldg(t.w_p + 8LL * e + m);
+  }
+  const double m0 = t.m0[e], m1 = t.m1[e];
+  double v[IL];
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1)
+      v[u] = m0 * interp16r(dut + (i0 + u) * srt, NPT, wt) + m1 * interp16r(dup + (i0 + u) * srp, NPP, wp);
+#pragma unroll
+  for (int u = 0; u < IL; ++u)
+    if (i0 + u <= i1) buf[((long long)s * g.nr + i0 + u) * t.n + e] = v[u];
 }
 template <int KTGT>
 __global__ void k_unpack_vec(Geo g, InterpArgs a, const double* __restrict__ buf) {
@@ -677,9 +696,10 @@ long long fringe_count(const Geo& g, const InterpArgs& a) {
 void launch_fringe_pack(const Geo& g, const InterpArgs& a, double* buf, cudaStream_t st) {
   double* bth = buf + 5LL * (g.nr + 1) * a.tab_cc.n;
   double* bph = bth + 2LL * g.nr * a.tab_th.n;
-  if (a.tab_cc.n) k_pack_cc<<<dim3((a.tab_cc.n + 127) / 128, g.nr + 1, 5), 128, 0, st>>>(g, a, buf);
-  if (a.tab_th.n) k_pack_vec<KT><<<dim3((a.tab_th.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bth);
-  if (a.tab_ph.n) k_pack_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, g.nr, 2), 128, 0, st>>>(g, a, bph);
+  const int ngc = (g.nr + 1 + IL - 1) / IL, ngv = (g.nr + IL - 1) / IL;
+  if (a.tab_cc.n) k_pack_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 5), 128, 0, st>>>(g, a, buf);
+  if (a.tab_th.n) k_pack_vec<KT><<<dim3((a.tab_th.n + 127) / 128, ngv, 2), 128, 0, st>>>(g, a, bth);
+  if (a.tab_ph.n) k_pack_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, ngv, 2), 128, 0, st>>>(g, a, bph);
 }
 
 void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, cudaStream_t st) {
