@@ -312,9 +312,20 @@ enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2, MODE_SLAB = 3 };
 // resident 128-thread blocks per SM the register allocation must allow (the
 // chunk arrays are 6 M registers): measured on B200 (C3), 96 registers for
 // chunks of <= 12 rows beat the unconstrained ~130 (occupancy over ILP)
+#ifndef YY_MINB_3212
+#define YY_MINB_3212 4      // phi lines of <= 384 rows: 128 registers, no spills (measured)
+#endif
+#ifndef YY_MINB_MW
+#define YY_MINB_MW 5
+#endif
+#ifndef YY_MINB_16
+#define YY_MINB_16 5        // r/theta (16, 6) / (16, 8) tiles
+#endif
 constexpr int line_minb(int P, int M) {
   return YY_LINE_MINB > 0 ? YY_LINE_MINB
-         : P > 32 ? (M <= 6 ? 5 : 4)      // multi-warp phi lines (part_solve3: 3 live arrays)
+         : P > 32 ? (M <= 6 ? YY_MINB_MW : 4)   // multi-warp phi lines (part_solve3: 3 live arrays)
+         : (P == 32 && M == 12) ? YY_MINB_3212
+         : (P == 16 && M <= 8) ? YY_MINB_16
                   : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 2 : 1);
 }
 
