@@ -181,10 +181,10 @@ template <int K> __device__ __forceinline__ double cotn(const Geo& g, int j) {  
 // Astar::av (RX = RX_SWEEP: line sweeps, RX_RESID: residuals; bit 3 Q + AX of the
 // masks) instead of averaging a* in place.  RX = 0 (static kernels): a* always.
 // Defaults measured on B200 (C3): every residual / sweep except the T residual
-// and the phi sweeps of T and u_r, whose in-place averages are as cheap.
+// and the phi sweep of T, whose in-place average is as cheap.
 enum { RX_NONE = 0, RX_SWEEP = 1, RX_RESID = 2, RX_GIVEN = 3 };   // GIVEN: adv / reaction passed in
 #ifndef YY_AV_SWEEP
-#define YY_AV_SWEEP 0xfdb
+#define YY_AV_SWEEP 0xffb
 #endif
 #ifndef YY_AV_RESID
 #define YY_AV_RESID 0xff8
