@@ -69,6 +69,21 @@ def test_plan_layout():
         dist.plan(8, 0, nr=96 + 2)       # 98 rows do not split into 4 slabs
 
 
+def test_c5_weak_scaling_layout():
+    """BASELINE C5 (bench.py --workload C5 at N GPUs): patch Nr = 64 N, a 128-row
+    slab per rank for N = 2, 4, 8, every slab solvable by the slab
+    chunk menu (n = P M: 128 = 16 x 8)."""
+    import workloads as W
+    from paper_1905_02300_b200 import dist
+    assert W.config("C5").nr == 64
+    for world in (2, 4, 8):
+        cfg = W.config("C5", G=world)
+        plans = [dist.plan(world, r, cfg.nr) for r in range(world)]
+        S = plans[0]["nslab"]
+        assert cfg.nr // S == 128 and S == world // 2
+        assert sorted((q["patch"], q["slab"]) for q in plans) == [(p, s) for p in (0, 1) for s in range(S)]
+
+
 def _fields_all(shells, p, lev, s):
     for sh in shells:
         if p in sh.patches:
