@@ -232,7 +232,8 @@ def run_yy(args):
     nsrc = len(wl["patches"][0]["sources"])
     forced = nsrc > 0
     stream = torch.cuda.Stream()
-    sh = Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, stream=stream.cuda_stream)
+    sh = Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, stream=stream.cuda_stream,
+               **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
     sh.load_workload(wl)
     W_ = max(3, args.warmup)
     for _ in range(W_):
@@ -337,7 +338,8 @@ def run_yy(args):
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
-                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra, "schwarz_tol": cfg.tol,
+                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra,
+                   "schwarz_tol": cfg.tol if not args.fixed_iters else f"fixed K = {args.fixed_iters}",
                    "schwarz_iters_per_step": Ks, "l2_flush": "inputs larger than L2 (working set ~37 fp64 fields)",
                    "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
                                      "model_bytes": model_bytes,
@@ -384,7 +386,7 @@ def run_yy_dist(args, rank, world, local):
     stream = torch.cuda.Stream()
     dist.plan(world, rank, cfg.nr)                 # validates the slab split
     sh = Shell.dist(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, world, rank, uid, local,
-                    stream=stream.cuda_stream)
+                    stream=stream.cuda_stream, **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
     sh.load_workload(wl)
     W_ = max(3, args.warmup)
     for _ in range(W_):
@@ -437,6 +439,8 @@ def main():
     ap.add_argument("--workload", default="C3", choices=("C1", "C2", "C3", "C5"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fixed-iters", type=int, default=0,
+                    help="Schwarz iterations per step fixed (the paper's scaling protocol, C5: 10); 0 = to tolerance")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
