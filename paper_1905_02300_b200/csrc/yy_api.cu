@@ -79,7 +79,8 @@ struct yy_ctx {
   double* Vq[4] = {};          // per quantity: the r-lines' responses to the lower / upper
   double* Wq[4] = {};          // neighbour slab's boundary unknown (per step)
   bool vw_fresh = true;        // this iteration writes Vq / Wq (the step's first)
-  double* IF = nullptr;        // [nlines][6] this slab's boundary rows
+  double* IFq[4] = {};         // per quantity: [nlines][6] this slab's boundary rows (x0 each
+                               // iteration; xlo, xhi columns per step, like Vq / Wq)
   double* IFall = nullptr;     // [nslab][nlines][6] every slab of the patch
   double* LH = nullptr;        // [nlines][2]
   double* gath = nullptr;      // [world][2 + 2 NSLOT] every context's sums
@@ -620,7 +621,7 @@ SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
   w.maxb = ctx->maxb;
   // radial slabs: V, W of quantity q's r-factor (one matrix per step, shared by
   // both systems) are written by the first iteration of the step only
-  w.V = ctx->Vq[q]; w.W = ctx->Wq[q]; w.IF = ctx->IF;
+  w.V = ctx->Vq[q]; w.W = ctx->Wq[q]; w.IF = ctx->IFq[q];
   w.vw = ctx->vw_fresh && (q == QT || s == 1);
   return w;
 }
@@ -663,7 +664,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
       for (int p = 0; p < 2; ++p)
         for (int a1 = 0; a1 < S && (cs[0]->mode == 2 || has_patch(cs, p)); ++a1)
           for (int b1 = 0; b1 < S; ++b1)
-            ops.push_back({p * S + a1, p * S + b1, [](yy_ctx* c) -> const double* { return c->IF; },
+            ops.push_back({p * S + a1, p * S + b1, [q](yy_ctx* c) -> const double* { return c->IFq[q]; },
                            [=](yy_ctx* c) { return c->IFall + (long long)a1 * nlines * 6; }, 6LL * nlines});
       TRY(run_xfers(cs, ops));
       for (yy_ctx* ctx : cs) {
@@ -964,12 +965,16 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     *rho_out = rho;
     return YY_OK;
   }
-  if (graph) {
+  // radial slabs: the step's first iteration also computes the slab coupling
+  // responses V / W; later ones solve for x0 alone — two graphs
+  cudaGraphExec_t gexec2 = nullptr;
+  const bool two = graph && cs[0]->nslab > 1;
+  auto capture = [&](bool fresh, cudaGraphExec_t* out) -> yy_status {
     cudaGraph_t gr = nullptr;
     std::vector<long long> l0(cs.size());
     for (size_t q = 0; q < cs.size(); ++q) {
       l0[q] = cs[q]->launches;
-      cs[q]->vw_fresh = true;      // (the replayed iteration also writes the slab V / W)
+      cs[q]->vw_fresh = fresh;
     }
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     yy_status sc = exchange_fringe(cs);
@@ -981,12 +986,20 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     const cudaError_t ec = cudaStreamEndCapture(ctx->st, &gr);
     if (sc != YY_OK) return sc;
     CK(ec);
-    const cudaError_t ei = cudaGraphInstantiate(&gexec, gr, 0);
+    const cudaError_t ei = cudaGraphInstantiate(out, gr, 0);
     cudaGraphDestroy(gr);
     CK(ei);
     for (size_t q = 0; q < cs.size(); ++q) {
       glaunches[q] = cs[q]->launches - l0[q];
       cs[q]->launches = l0[q];
+    }
+    return YY_OK;
+  };
+  if (graph) {
+    TRY(capture(true, &gexec));
+    if (two) {
+      const yy_status s2 = capture(false, &gexec2);
+      if (s2 != YY_OK) { cudaGraphExecDestroy(gexec); return s2; }
     }
   }
   while (k < kmax) {
@@ -994,8 +1007,12 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     if (!graph)
       for (yy_ctx* c : cs) c->vw_fresh = (k == 1);   // slab V / W: once per step (the step's matrices)
     if (graph) {
-      const cudaError_t el = cudaGraphLaunch(gexec, ctx->st);
-      if (el != cudaSuccess) { cudaGraphExecDestroy(gexec); CK(el); }
+      const cudaError_t el = cudaGraphLaunch((k == 1 || !two) ? gexec : gexec2, ctx->st);
+      if (el != cudaSuccess) {
+        cudaGraphExecDestroy(gexec);
+        if (gexec2) cudaGraphExecDestroy(gexec2);
+        CK(el);
+      }
       for (size_t q = 0; q < cs.size(); ++q) cs[q]->launches += glaunches[q];
     } else if (ctx->schwarz == 1) {                        // multiplicative: Yin, then Yang with Yin's k
       for (int p = 0; p < 2; ++p) {
@@ -1025,12 +1042,14 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     rho = ctx->red_host[0];
     if (ctx->red_host[1] != 0.0) {
       if (gexec) cudaGraphExecDestroy(gexec);
+      if (gexec2) cudaGraphExecDestroy(gexec2);
       for (yy_ctx* c : cs) fail(c, YY_ESOLVER, "NaN/Inf in the Schwarz residual");
       return YY_ESOLVER;
     }
     if (ctx->fixed_iters <= 0 && rho < tol) break;
   }
   if (gexec) cudaGraphExecDestroy(gexec);
+  if (gexec2) cudaGraphExecDestroy(gexec2);
   for (yy_ctx* c : cs) step_end(c);
   *iters = k;
   *rho_out = rho;
@@ -1247,7 +1266,9 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
         return s;
       }
     if (
-        (s = dalloc(ctx, &ctx->IF, 6 * nlmax)) != YY_OK || (s = dalloc(ctx, &ctx->IFall, 6 * nslab * nlmax)) != YY_OK ||
+        (s = dalloc(ctx, &ctx->IFq[0], 6 * nlmax)) != YY_OK || (s = dalloc(ctx, &ctx->IFq[1], 6 * nlmax)) != YY_OK ||
+        (s = dalloc(ctx, &ctx->IFq[2], 6 * nlmax)) != YY_OK || (s = dalloc(ctx, &ctx->IFq[3], 6 * nlmax)) != YY_OK ||
+        (s = dalloc(ctx, &ctx->IFall, 6 * nslab * nlmax)) != YY_OK ||
         (s = dalloc(ctx, &ctx->LH, 2 * nlmax)) != YY_OK) { yy_destroy(ctx); return s; }
   }
   ctx->rank = patch0 * nslab + slab;

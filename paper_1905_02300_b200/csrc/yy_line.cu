@@ -569,12 +569,23 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
 #pragma unroll
       for (int u = 0; u < M; ++u) RH[o + u] = rh[u] + lo[u] * XL + up[u] * XH;
     } else if constexpr (MODE == MODE_SLAB) {
-      part_solve3<P, M>(lo, up, rh, c);
+      if (a.vw) {
+        // the step's first iteration: x0 and the responses xlo, xhi to the
+        // neighbour slabs' boundary unknowns (per step: they depend on the matrix only)
+        part_solve3<P, M>(lo, up, rh, c);
 #pragma unroll
-      for (int u = 0; u < M; ++u) {
-        RH[o + u] = rh[u];
-        LO[o + u] = lo[u];
-        UP[o + u] = up[u];
+        for (int u = 0; u < M; ++u) {
+          RH[o + u] = rh[u];
+          LO[o + u] = lo[u];
+          UP[o + u] = up[u];
+        }
+      } else {
+        // later iterations: x0 alone (the couplings to the neighbour slabs zero)
+        if (c == 0) lo[0] = 0.0;
+        if (c == P - 1) up[M - 1] = 0.0;
+        part_solve<P, M>(lo, up, rh, c);
+#pragma unroll
+        for (int u = 0; u < M; ++u) RH[o + u] = rh[u];
       }
     } else {
       part_solve<P, M>(lo, up, rh, c);
@@ -640,18 +651,16 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
         const double r = rnode<K>(g, i), s = snode<K>(g, j);
         wsum += r * r * s * x * x;
       } else if (MODE == MODE_SLAB) {
-        const double xl = LO[slot(l, e)], xh = UP[slot(l, e)];
         R[nd] = x;
-        if (a.vw) {                           // (per-step: the line's responses to its couplings)
+        double* f = (e == 0 || e == n - 1)    // this slab's boundary rows of the line
+                        ? a.IF + 6LL * ((j - 1) * (NPk(g, K) - 2) + (k - 1)) + (e == 0 ? 0 : 3) : nullptr;
+        if (a.vw) {                           // (per step: the line's responses to its couplings)
+          const double xl = LO[slot(l, e)], xh = UP[slot(l, e)];
           a.V[po + nd] = xl;
           a.W[po + nd] = xh;
+          if (f) { f[1] = xl; f[2] = xh; }
         }
-        if (e == 0 || e == n - 1) {           // this slab's boundary rows of the line
-          double* f = a.IF + 6LL * ((j - 1) * (NPk(g, K) - 2) + (k - 1)) + (e == 0 ? 0 : 3);
-          f[0] = x;
-          f[1] = xl;
-          f[2] = xh;
-        }
+        if (f) f[0] = x;
       } else {
         R[nd] = x;
       }
