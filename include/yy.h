@@ -119,8 +119,9 @@ yy_status yy_create_dist(const yy_grid* g, double R1, double R2, double Pr, doub
 yy_status yy_nccl_unique_id(void* out128);
 
 /* Set one patch's state.  level 0 = t^n, 1 = t^{n-1} (p ignored).  system
- * 0 = both bootstrapped systems (u1 = u2, p1 = p2; eq:ac1/eq:ac2), 1 or 2 =
- * that system only.  T is shared by both systems. */
+ * 0 = both bootstrapped systems (u1 = u2, p1 = p2; eq:ac1/eq:ac2; one host copy,
+ * system 2 filled by device copies), 1 or 2 = that system only.  T is shared
+ * by both systems.  NULL members are left unchanged. */
 yy_status yy_set_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system,
                         const yy_fields* f);
 

@@ -1385,6 +1385,23 @@ yy_status yy_set_fields(yy_ctx* ctx, int32_t patch, int32_t level, int32_t syste
   };
   for (int s = sys_lo; s <= sys_hi; ++s) {
     const int o = (s == 2) ? 3 : 0;
+    if (s == 2 && system == 0) {
+      // both systems from one host copy: system 2's arrays are device copies of
+      // system 1's (the same patch window)
+      auto dup = [&](int f1, int f2, const double* src) -> yy_status {
+        if (!src) return YY_OK;
+        const long long sz = fsize(ctx, f1);
+        CK(cudaMemcpyAsync(L[f2] + (patch - ctx->patch0) * sz, L[f1] + (patch - ctx->patch0) * sz,
+                           sz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+        return YY_OK;
+      };
+      TRY(dup(FUR1, FUR2, f->ur));
+      TRY(dup(FUT1, FUT2, f->ut));
+      TRY(dup(FUP1, FUP2, f->up));
+      if (level == 0) TRY(dup(FP1, FP2, f->p));
+      CK(cudaStreamSynchronize(ctx->st));
+      continue;
+    }
     TRY(put(FUR1 + o, f->ur));
     TRY(put(FUT1 + o, f->ut));
     TRY(put(FUP1 + o, f->up));

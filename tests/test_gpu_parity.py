@@ -295,6 +295,24 @@ def test_max_iters_reports_no_convergence(graph):
         os.environ.pop("YY_GRAPH", None)
 
 
+def test_set_fields_system0_is_both_systems():
+    """yy_set_fields(system = 0) fills both systems from one host copy (system 2
+    by device copies): the same state as two separate uploads."""
+    cfg = W.small("C1", 5, 12, 30, dt=1e-3)
+    wl = W.random_state(cfg, seed=7, amp=1.0)
+    a, b = _shell(cfg), _shell(cfg)
+    for p, pd in enumerate(wl["patches"]):
+        n = pd["n"]
+        a.set_fields(p, 0, 1, ur=n["ur"], ut=n["ut"], up=n["up"], T=n["T"], p=n["p1"])
+        a.set_fields(p, 0, 2, ur=n["ur"], ut=n["ut"], up=n["up"], p=n["p1"])
+        b.set_fields(p, 0, 0, ur=n["ur"], ut=n["ut"], up=n["up"], T=n["T"], p=n["p1"])
+    for p in range(2):
+        for s in (1, 2):
+            fa, fb = a.get_fields(p, 0, s), b.get_fields(p, 0, s)
+            for k in fa:
+                assert np.array_equal(fa[k], fb[k]), (p, s, k)
+
+
 def test_errors_are_reported():
     from paper_1905_02300_b200 import YYError
     cfg = W.small("C1", 4, 12, 28)
