@@ -20,10 +20,10 @@ timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__tim
 echo "ncu1 rc $?" >> gpurun_out/rc.txt
 python tools/ncu_launches.py gpurun_out/launches.csv > gpurun_out/launches.md 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"k_line|k_resid|k_pres|k_interp" -s 3000 -c 40 -o /tmp/prof_iter $B > gpurun_out/ncu2.log 2>&1
+  -k regex:"k_line|k_resid|k_pres|k_interp" -s 3000 -c 40 -f -o /tmp/prof_iter $B > gpurun_out/ncu2.log 2>&1
 echo "ncu2 rc $?" >> gpurun_out/rc.txt
 python tools/ncu_full_summary.py /tmp/prof_iter.ncu-rep > gpurun_out/ncu_full.md 2>&1
 python tools/ncu_traffic.py /tmp/prof_iter.ncu-rep "${LABEL:-}" > gpurun_out/traffic.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"k_resid<.int.3, .int.2" -s 40 -c 1 -o gpurun_out/prof_top $B > gpurun_out/ncu3.log 2>&1
+  -k regex:"k_resid<.int.3, .int.2" -s 40 -c 1 -f -o gpurun_out/prof_top $B > gpurun_out/ncu3.log 2>&1
 echo "ncu3 rc $?" >> gpurun_out/rc.txt
