@@ -25,7 +25,7 @@ def _shell(cfg, **kw):
     return Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, **kw)
 
 
-@pytest.mark.parametrize("name,steps", [("C2", 1), ("C3", 1), ("C5", 1), ("C3", 3)])
+@pytest.mark.parametrize("name,steps", [("C2", 1), ("C3", 1), ("C5", 1), ("C3", 3), ("C2", 5)])
 def test_full_size_steps_match_oracle_golden(name, steps):
     """Full BASELINE size, the bench launch configuration: `steps` steps from the
     workload's initial state; every step's Schwarz count equal; sampled nodes
