@@ -329,8 +329,9 @@ class Shell:
             if patch not in self.patches:
                 continue
             n = pd["n"]
-            self.set_fields(patch, 0, 1, ur=n["ur"], ut=n["ut"], up=n["up"], T=n["T"], p=n["p1"])
-            self.set_fields(patch, 0, 2, ur=n["ur"], ut=n["ut"], up=n["up"], p=n["p2"])
+            # both systems from one host copy of u (u1 = u2 at the start), then p2
+            self.set_fields(patch, 0, 0, ur=n["ur"], ut=n["ut"], up=n["up"], T=n["T"], p=n["p1"])
+            self.set_fields(patch, 0, 2, p=n["p2"])
             m = pd["nm1"]
             self.set_fields(patch, 1, 0, **{k: m[k] for k in ("ur", "ut", "up", "T")})
             self.set_wall(patch, pd["walls"])
