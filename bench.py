@@ -189,6 +189,48 @@ def dist_env():
     return rank, world, local
 
 
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: launch the N ranks ourselves, exactly
+    as the driver's `python -m torch.distributed.run --nnodes=1 --nproc-per-node N
+    --master-addr 127.0.0.1` would, after checking that N devices exist (fails
+    loudly otherwise: a silent one-GPU run would mislabel the result)."""
+    if not args.launch_check:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_launch_check(args):
+    """Rank plumbing only (no GPU): every rank joins a gloo group, the ranks agree
+    on the world size and the max-over-ranks reduction the timed path uses."""
+    import torch
+    import torch.distributed as td
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    td.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    td.all_reduce(t, op=td.ReduceOp.MAX)
+    ranks = [None] * world
+    td.all_gather_object(ranks, rank)
+    if rank == 0:
+        emit({"launch_check": True, "world": world, "n_gpus": args.gpus, "ranks": ranks, "max_over_ranks": float(t)})
+    td.destroy_process_group()
+    return 0
+
+
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
@@ -207,7 +249,7 @@ def run_reference(args):
     v = tot_cells / tot_sec
     sample = (f"{args.workload} physics on a {grid[0]}x{grid[1]}x{grid[2]} per-patch grid (1/{SAMPLE_DIV[args.workload] ** 3} "
               f"of the cells), one full time step per bench step, mean Schwarz K={statistics.mean(s[2] for s in steps):.1f}")
-    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": max(world, args.gpus),
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_sec / len(steps),
           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
           "data": "synthetic", "config": {"workload": args.workload, "sample": sample},
@@ -224,6 +266,9 @@ def run_yy(args):
     from paper_1905_02300_b200 import Shell
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus} (launch with torchrun, or "
+                         "without WORLD_SIZE to let bench.py start the ranks)")
     if world > 1:
         return run_yy_dist(args, rank, world, local)
     torch.cuda.set_device(local)
@@ -442,9 +487,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fixed-iters", type=int, default=0,
                     help="Schwarz iterations per step fixed (the paper's scaling protocol, C5: 10); 0 = to tolerance")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)   # CPU test of the rank launch
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if args.launch_check:
+        return run_launch_check(args)
     return run_yy(args)
 
 

@@ -44,21 +44,32 @@ class Oracle:
     """Both patches of one shell, stepped with plain numpy."""
 
     def __init__(self, nr, nth, nph, R1, R2, Pr, Ra, dt, chi=1.0, max_iters=100, fixed_iters=0,
-                 factor_order=None, schwarz="additive", flux_fix_eps=None):
+                 factor_order=None, schwarz="additive", flux_fix_eps=None, advection="split"):
         self.g = Grid(nr, nth, nph, R1, R2)
         self.prm = Params(Pr, Ra, dt, chi)
         self.ex = Exchange(self.g)
         self.max_iters = max_iters
         self.fixed_iters = fixed_iters
-        if schwarz not in ("additive", "multiplicative"):
+        if schwarz not in ("additive", "multiplicative", "none"):
             raise ValueError(schwarz)
         # additive (RD26): both patches take the other's iterate k-1.  multiplicative
         # (Algorithm 1 as printed, P:L487-513): Yin first with Yang's iterate k-1,
-        # then Yang with Yin's fresh iterate k (SURVEY NEXT-1).
+        # then Yang with Yin's fresh iterate k (SURVEY NEXT-1).  none: no exchange —
+        # each patch is a single domain whose fringe keeps the Dirichlet values it
+        # holds (Theorem 1's setting, P:L250-260: one simply shaped domain).
         self.schwarz = schwarz
         # Algorithm 1 step 4 (optional in the paper, P:L515-517): None = off (SURVEY NEXT-4)
         self.flux_fix_eps = flux_fix_eps
         self.order = dict(FACTOR_ORDER) if factor_order is None else factor_order
+        # where the linearised advection goes (P:L103-107): "split" = inside the
+        # direction-wise factors (the paper's scheme, eq:Convect_Douglas and
+        # eq:r_comp..phi_comp); "imex" = the IMEX alternative (SURVEY NEXT-3): the
+        # split operators are the a* = 0 rows (diffusion, metric, grad-div), the
+        # transport terms (advection and the a*-reaction terms of RD14 / P:L444)
+        # stay only in the explicit L_full psi^* of G (AB2-extrapolated)
+        if advection not in ("split", "imex"):
+            raise ValueError(advection)
+        self.imex = advection == "imex"
         self.t = 0.0
         g = self.g
         z = lambda k: np.zeros(g.shape(k))
@@ -136,7 +147,11 @@ class Oracle:
         """Directional weights, cached per step (a* is fixed for the whole step)."""
         key = (id(astar), q, axis, hat)
         if key not in self._cc:
-            self._cc[key] = ops.coeffs(self.g, self.prm, q, axis, hat, astar)
+            if hat and self.imex:
+                a0 = [np.zeros(self.g.shape(k)) for k in ("R", "TH", "PH")]
+                self._cc[key] = ops.coeffs(self.g, self.prm, q, axis, hat, a0)
+            else:
+                self._cc[key] = ops.coeffs(self.g, self.prm, q, axis, hat, astar)
         return self._cc[key]
 
     def L(self, q, X, W, hat, astar):
@@ -288,6 +303,17 @@ class Oracle:
                 for p in range(2):
                     self._fill_fringe(p, cur, wnew)
                     self._flux_fix(p, cur, tol)
+                    rho = max(rho, self._iterate_patch(p, cur[p], stat[p], wdiff[p]))
+                if not self.fixed_iters and rho < tol:
+                    break
+                continue
+            if self.schwarz == "none":
+                for p in range(2):
+                    for s_ in (1, 2):
+                        cur[p][f"ur{s_}"][0] = wnew[p]["ur"][0]
+                        cur[p][f"ur{s_}"][-1] = wnew[p]["ur"][1]
+                rho = 0.0
+                for p in range(2):
                     rho = max(rho, self._iterate_patch(p, cur[p], stat[p], wdiff[p]))
                 if not self.fixed_iters and rho < tol:
                     break

@@ -54,3 +54,19 @@ def test_main_arm_line():
     assert c["sm_mhz"] > 0 and isinstance(c["reasons"], list)
     assert d["gpu_launches"] > 0
     assert len(d["config"]["schwarz_iters_per_step"]) == 3
+
+
+def test_gpus_flag_launches_the_ranks():
+    # `bench.py --gpus 2` without torchrun starts 2 ranks itself (gloo plumbing
+    # check on CPU: every rank sees WORLD_SIZE = 2 and takes part in the
+    # max-over-ranks reduction of the timed path)
+    d = _run("--gpus", "2", "--launch-check", timeout=300)
+    assert d["launch_check"] is True and d["world"] == 2 and d["n_gpus"] == 2
+    assert sorted(d["ranks"]) == [0, 1] and d["max_over_ranks"] == 2.0
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1 but --gpus 2" in out.stderr

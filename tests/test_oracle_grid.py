@@ -119,3 +119,39 @@ def test_exchange_cubic_exact_and_rigid_vector():
         m2 = ~gg.solved_mask("PH")
         errs.append(max(np.max(np.abs(t_ut - s[0]["ut"])[m]), np.max(np.abs(t_up - s[0]["up"])[m2])))
     assert errs[0] < 1e-3 and errs[1] < errs[0] / 8
+
+
+def _box_volume(R1, R2, ta, tb, pa, pb):
+    """int_{R1}^{R2} int_{ta}^{tb} int_{pa}^{pb} r^2 sin(th) dph dth dr (closed form)."""
+    return (R2 ** 3 - R1 ** 3) / 3.0 * (math.cos(ta) - math.cos(tb)) * (pb - pa)
+
+
+def test_weights_omega_midpoint_rule():
+    # RD24 / P:L559-560 ("standard mid-point approximation to the L2 norm"): the
+    # omega weights of one patch's cell centres are the midpoint rule for
+    # int r^2 sin(th) dr dth dph over the patch box.  The midpoint sums have closed
+    # forms (sum_i r_i^2 dr = (R2^3-R1^3)/3 - (R2-R1) dr^2/12 exactly; sum_j
+    # sin(th_j) dth = (cos a - cos b) (dth/2)/sin(dth/2) exactly), so the weights
+    # are pinned to rounding — a dropped r^2 or sin(th), a wrong cell width or a
+    # half-cell node offset fails — and the sum converges to the box integral.
+    # Over the full shell r in [1,2], th in [0,pi], ph in [0,2pi) the integral is
+    # ||1||^2_omega = 28 pi / 3 (S:L181).
+    assert abs(_box_volume(1.0, 2.0, 0.0, math.pi, 0.0, 2 * math.pi) - 28 * math.pi / 3) < 1e-13
+    for n in (1, 2, 4):
+        for R1, R2 in ((1.0, 2.0), (0.5, 3.0)):
+            g = Grid(6 * n, 12 * n, 28 * n, R1, R2)
+            S = float(np.sum(g.weights_omega("C")))
+            ta, pa = g.x0[1], g.x0[2]
+            tb, pb = ta + g.nth * g.dth, pa + g.nph * g.dph
+            mid_r = (R2 ** 3 - R1 ** 3) / 3.0 - (R2 - R1) * g.dr ** 2 / 12.0
+            mid_t = (math.cos(ta) - math.cos(tb)) * (0.5 * g.dth) / math.sin(0.5 * g.dth)
+            assert abs(S - mid_r * mid_t * (pb - pa)) < 1e-13 * S
+            exact = _box_volume(R1, R2, ta, tb, pa, pb)
+            assert abs(S - exact) / exact < (g.dr / (R2 - R1)) ** 2 + g.dth ** 2
+    # the other node kinds: nonnegative, and they integrate the same box at O(h)
+    g = Grid(24, 48, 112, 1.0, 2.0)
+    exact = _box_volume(1.0, 2.0, g.x0[1], g.x0[1] + g.nth * g.dth, g.x0[2], g.x0[2] + g.nph * g.dph)
+    for kind in ("R", "TH", "PH"):
+        w = g.weights_omega(kind)
+        assert np.all(w >= 0)
+        assert abs(float(np.sum(w)) - exact) / exact < 0.1
