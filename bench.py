@@ -169,7 +169,7 @@ def oracle_sample_step(cfg_name):
     full = W.config(cfg_name)
     d = SAMPLE_DIV[cfg_name]
     c = W.small(cfg_name, full.nr // d, full.nth // d, full.nph // d)
-    o = Oracle(c.nr, c.nth, c.nph, c.R1, c.R2, c.Pr, c.Ra, c.dt)
+    o = Oracle(c.nr, c.nth, c.nph, c.R1, c.R2, c.Pr, c.Ra, c.dt, chi=c.chi)
     o.load_workload(W.make_workload(c))
     t0 = time.perf_counter()
     o.step(1, c.tol)
@@ -278,7 +278,7 @@ def run_yy(args):
     forced = nsrc > 0
     stream = torch.cuda.Stream()
     sh = Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, stream=stream.cuda_stream,
-               **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
+               chi=cfg.chi, **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
     sh.load_workload(wl)
     W_ = max(3, args.warmup)
     for _ in range(W_):
@@ -384,7 +384,7 @@ def run_yy(args):
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
-                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra,
+                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra, "chi": cfg.chi,
                    "schwarz_tol": cfg.tol if not args.fixed_iters else f"fixed K = {args.fixed_iters}",
                    "schwarz_iters_per_step": Ks, "l2_flush": "inputs larger than L2 (working set ~37 fp64 fields)",
                    "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
@@ -432,7 +432,8 @@ def run_yy_dist(args, rank, world, local):
     stream = torch.cuda.Stream()
     dist.plan(world, rank, cfg.nr)                 # validates the slab split
     sh = Shell.dist(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, world, rank, uid, local,
-                    stream=stream.cuda_stream, **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
+                    stream=stream.cuda_stream, chi=cfg.chi,
+                    **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
     sh.load_workload(wl)
     W_ = max(3, args.warmup)
     for _ in range(W_):

@@ -66,10 +66,19 @@ enum {
   YY_SCHWARZ = 5,      /* 0: additive (RD26, default); 1: multiplicative, Algorithm 1 as printed
                           (Yin with Yang's iterate k-1, then Yang with Yin's k).
                           Needs one patch per context (yy_create_dist, or the test-only
-                          yy_create_pair / yy_create_slabs); set on every rank            */
+                          yy_create_pair / yy_create_slabs); set on every rank.
+                          2: none — every patch is a single domain whose fringe keeps the
+                          Dirichlet values set by yy_set_fields (Theorem 1's setting,
+                          P:L250-260; with YY_HEAT_ONLY and YY_FIXED_ITERS = 1 a step is
+                          exactly eq:HeatDouglas)                                          */
   YY_HEAT_ONLY = 6,    /* !=0: the heat Douglas scheme eq:HeatDouglas alone: only
                           T is solved (u, p stay as set, normally 0 so a* = 0), the
                           momentum and pressure kernels are skipped, rho_k is T's norm      */
+  YY_ADVECTION = 9,    /* where the linearised advection goes: 0 = inside the
+                          direction-wise factors (the paper's scheme, default); 1 = IMEX (SURVEY
+                          NEXT-3): the factors and L_split are the a* = 0 rows (diffusion,
+                          metric, grad-div), the transport terms (advection, the a*-reaction
+                          terms of RD14 / P:L444) stay only in the explicit L_full psi^* of G */
   YY_INTERP_ORDER = 8, /* fringe interpolation order: 4 (4x4 Lagrange in (theta, phi), RD4) is the
                           only one built; any other value is YY_EINVAL                       */
   YY_FLUX_FIX = 7      /* eps > 0: Algorithm 1 step 4 every
@@ -167,6 +176,19 @@ yy_status yy_get_stats(const yy_ctx* ctx, int32_t cap, int32_t* iters_per_step,
                        double* resid_per_step, int32_t* n_out);
 
 double yy_time(const yy_ctx* ctx);
+
+/* Theorem 1 diagnostic (eq:Stability; DESIGN.md §8 NEXT-2): for the
+ * current levels T^n, T^{n-1} of every patch the context holds, with u = 0 rows
+ * (pure diffusion) and HOMOGENEOUS wall / fringe data (the theorem's setting;
+ * the stored fringe values must be 0 for the identity to hold), out3 (host, 3
+ * doubles) = { 1/2 (-L T^n, T^n)_w,  1/4 (-(Lh - L) dT, dT)_w,  (dT, dT)_w },
+ * dT = T^n - T^{n-1}, L the full and Lh the hat (theta, phi) operators of
+ * P:L208, (.,.)_w the midpoint omega inner product over solved cell centres
+ * (RD24).  The left side of eq:Stability after step N is
+ * sum_{n<=N} out3[2]/tau + out3[0] + out3[1]: non-increasing in N for the
+ * heat-only single-domain Douglas scheme.  Whole patches only (no radial slabs:
+ * YY_EINVAL).  Synchronous with respect to the host. */
+yy_status yy_energy(yy_ctx* ctx, double* out3);
 
 /* Number of CUDA kernels this context has launched since creation. */
 int64_t yy_launch_count(const yy_ctx* ctx);

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -60,7 +61,11 @@ struct yy_ctx {
   // contexts in one process sharing a stream, test path); 2: NCCL, one rank per patch.
   int patch0 = 0;
   int nslab = 1, slab = 0, roff = 0, nr_glob = 0;   // radial slab of the patch (nslab > 1)
-  int schwarz = 0;             // 0 additive (RD26), 1 multiplicative (Algorithm 1 as printed)
+  int schwarz = 0;             // 0 additive (RD26), 1 multiplicative (Algorithm 1 as printed),
+                               // 2 none (single domains, Theorem 1)
+  double* energy_buf = nullptr;   // yy_energy: zero wall + block partials + result
+  bool imex = false;           // YY_ADVECTION = 1: transport terms explicit only
+  double* zero = nullptr;      // IMEX: zero a* / row-weight / reaction arrays of the split rows
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
   double* bsplit[4][3] = {};   // split-row tables (Geo::bsplit)
@@ -112,6 +117,8 @@ struct yy_ctx {
   int wtf[2][MAXSRC] = {};
   double* wl[3][NW] = {};       // wall data at t_{n-1}, t_n, t_{n+1}
   double* sterm[2][MAXSRC][4] = {};
+  double* wterm_buf[2][MAXSRC][NW] = {};   // owned buffers behind wterm / sterm (reused by re-sets)
+  double* sterm_buf[2][MAXSRC][4] = {};
   int ns[2] = {0, 0};
   int stf[2][MAXSRC] = {};
   // interpolation tables (device)
@@ -182,13 +189,16 @@ cudaEvent_t ev_get(yy_ctx* ctx) {
   return e;
 }
 
+const char* kname(const std::string& s);
+
 struct ProfScope {   // brackets one or more launches of one kernel class
   yy_ctx* ctx;
   yy_ctx::Rec r{};
-  ProfScope(yy_ctx* c, const char* name, int nlaunch) : ctx(c) {
+  // the class name is interned only when the per-class profile is on
+  ProfScope(yy_ctx* c, const std::string& name, int nlaunch) : ctx(c) {
     ctx->launches += nlaunch;
     if (ctx->prof_on) {
-      r.name = name;
+      r.name = kname(name);
       r.a = ev_get(ctx);
       r.b = ev_get(ctx);
       cudaEventRecord(r.a, ctx->st);
@@ -218,7 +228,9 @@ void prof_collect(yy_ctx* ctx) {   // call after a stream synchronisation
 const char* QNAME[4] = {"T", "ur", "ut", "up"};
 const char* AXNAME[3] = {"r", "th", "ph"};
 std::string g_names_store[512];
-const char* kname(const std::string& s) {   // interned kernel-class names
+std::mutex g_names_mu;
+const char* kname(const std::string& s) {   // interned kernel-class names (process-wide, locked)
+  std::lock_guard<std::mutex> lk(g_names_mu);
   for (auto& x : g_names_store) {
     if (x == s) return x.c_str();
     if (x.empty()) { x = s; return x.c_str(); }
@@ -396,7 +408,12 @@ yy_status copy_window(yy_ctx* ctx, int K, double* dev_patch, double* host, bool 
   const size_t bytes = (size_t)(g1 - g0 + 1) * plane * sizeof(double);
   double* d = dev_patch + (long long)(g0 - ctx->roff) * plane;
   double* hh = host + (long long)g0 * plane;
-  CK(to_device ? cudaMemcpy(d, hh, bytes, cudaMemcpyHostToDevice) : cudaMemcpy(hh, d, bytes, cudaMemcpyDeviceToHost));
+  // on the context's stream, then synchronised: every upload / download is ordered
+  // with the step's kernels and with the device-to-device copies of yy_set_fields
+  // (system 0), whatever stream the caller uses; pageable host memory is safe too
+  CK(cudaMemcpyAsync(to_device ? (void*)d : (void*)hh, to_device ? (const void*)hh : (const void*)d, bytes,
+                     to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
   return YY_OK;
 }
 
@@ -434,6 +451,7 @@ yy_status eval_walls(yy_ctx* ctx, int L, double t) {
 
 StaticArgs static_args(yy_ctx* ctx, int q, double tsrc) {
   StaticArgs a{};
+  a.imex = ctx->imex;
   a.ar = ctx->astar[0]; a.at = ctx->astar[1]; a.ap = ctx->astar[2];
   a.rt = ctx->react_t; a.rp = ctx->react_p;
   const int f1 = (q == QT) ? FT : (q == QUR ? FUR1 : q == QUT ? FUT1 : FUP1);
@@ -601,6 +619,7 @@ ResidArgs resid_args(yy_ctx* ctx, int q, int s) {
   r.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
   r.ar = ctx->astar[0]; r.at = ctx->astar[1]; r.ap = ctx->astar[2];
   r.rt = ctx->react_t; r.rp = ctx->react_p;
+  if (ctx->imex) r.ar = r.at = r.ap = r.rt = r.rp = ctx->zero;   // split rows without transport terms
   r.G = ctx->G[f];
   r.R = ctx->R;
   r.Tit = ctx->it[FT]; r.Tn = ctx->n[FT];
@@ -616,6 +635,7 @@ SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
   SweepArgs w{};
   w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
   w.rt = ctx->react_t; w.rp = ctx->react_p;
+  if (ctx->imex) w.ar = w.at = w.ap = w.rt = w.rp = ctx->zero;
   w.R = ctx->R; w.psi = ctx->it[qfield(q, s)];
   w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
   w.maxb = ctx->maxb;
@@ -642,7 +662,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
     if (ctx->fuse) continue;
     ResidArgs r = resid_args(ctx, q, s);
     r.rev = next_order(ctx);
-    ProfScope ps(ctx, kname(rname), 1);
+    ProfScope ps(ctx, rname, 1);
     launch_resid(ctx->g, q, s, r, ctx->st);
   }
   const int S = cs[0]->nslab;
@@ -656,7 +676,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
       const int K = kind_of(q), nlines = (NTk(g, K) - 2) * (NPk(g, K) - 2);
       for (yy_ctx* ctx : cs) {
         SweepArgs w = sweep_args(ctx, q, s, slot);
-        ProfScope ps(ctx, kname(cls + "_slab"), 1);
+        ProfScope ps(ctx, cls + "_slab", 1);
         const int nb = launch_sweep(ctx->g, q, ax, s, false, false, true, w, nullptr, 1, ctx->st);
         if (nb < 0) return fail(ctx, YY_ESTATE, "radial slab lines must fill the line chunks (nr / nslab)");
       }
@@ -670,7 +690,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
       for (yy_ctx* ctx : cs) {
         SweepArgs w = sweep_args(ctx, q, s, slot);
         SlabArgs sa{ctx->IFall, ctx->LH, S, ctx->slab, nlines};
-        ProfScope ps(ctx, kname(cls + "_couple"), 2);
+        ProfScope ps(ctx, cls + "_couple", 2);
         launch_slab_solve(sa, ctx->st);
         const int nb = launch_slab_correct(ctx->g, K, fin, w, ctx->LH, ctx->st);
         if (fin) ctx->nblk[slot] = nb;
@@ -681,7 +701,7 @@ yy_status solve_quantity(std::vector<yy_ctx*>& cs, int q, int s, int slot) {
       ResidArgs r = resid_args(ctx, q, s);
       SweepArgs w = sweep_args(ctx, q, s, slot);
       w.rev = next_order(ctx);
-      ProfScope ps(ctx, kname(cls), 1);
+      ProfScope ps(ctx, cls, 1);
       const int nb = launch_sweep(ctx->g, q, ax, s, first, fin, false, w, first ? &r : nullptr, ctx->g.npatch,
                                   ctx->st);
       if (nb < 0) return fail(ctx, YY_ESTATE, "internal: no sweep kernel for this factor");
@@ -707,7 +727,7 @@ yy_status step_begin(yy_ctx* ctx) {
     ProfScope ps(ctx, "astar", 1);
     launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
   }
-  {
+  if (!ctx->imex) {   // IMEX: the split rows take no transport terms (Geo::adv -> zero)
     ProfScope ps(ctx, "react", 1);
     launch_react(g, ctx->astar[0], ctx->astar[1], ctx->react_t, ctx->react_p, st);
     launch_adv(g, ctx->astar[0], ctx->astar[1], ctx->astar[2], ctx->adv, NPT, st);
@@ -715,7 +735,7 @@ yy_status step_begin(yy_ctx* ctx) {
   // O3: static right-hand sides
   for (int q = 0; q < (ctx->heat_only ? 1 : 4); ++q) {
     StaticArgs a = static_args(ctx, q, t + 0.5 * tau);
-    ProfScope ps(ctx, kname(std::string("static_") + QNAME[q]), 1);
+    ProfScope ps(ctx, std::string("static_") + QNAME[q], 1);
     launch_static(g, q, a, st);
   }
   // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
@@ -790,6 +810,7 @@ yy_status iter_solve(std::vector<yy_ctx*>& cs) {
 // O5 for target patch p only (multiplicative Schwarz): the other patch's contexts
 // evaluate p's fringe from their current iterate, p's contexts write it
 yy_status exchange_fringe_to(std::vector<yy_ctx*>& cs, int p) {
+  if (cs[0]->schwarz == 2) return YY_OK;                 // single domains: no exchange
   const int S = cs[0]->nslab;
   for (yy_ctx* ctx : cs) {
     if (ctx->patch0 != 1 - p) continue;
@@ -812,6 +833,9 @@ yy_status exchange_fringe_to(std::vector<yy_ctx*>& cs, int p) {
 
 // O5 (N3): fringe of every patch from the other patch's iterate k-1
 yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
+  // YY_SCHWARZ = 2: every patch a single domain whose fringe keeps its Dirichlet
+  // values (Theorem 1's setting)
+  if (cs[0]->schwarz == 2) return YY_OK;
   if (!distributed(cs)) {
     yy_ctx* ctx = cs[0];
     ProfScope ps(ctx, "interp", 3);
@@ -905,8 +929,17 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   // replay it — the ~35 kernels then follow each other without per-launch gaps.
   // graphs: one context (mode 0) or a loopback group on one shared stream
   // (mode 1, additive Schwarz); NCCL ranks (mode 2) launch stream by stream
+  // NCCL ranks (mode 2): the iteration with its grouped ncclSend / ncclRecv captured
+  // into one graph per iteration kind when YY_DIST_GRAPH=1 (NCCL >= 2.9 supports
+  // stream capture of point-to-point calls; off by default: this round's boxes
+  // have one GPU, so the captured NCCL path has not run)
+  static const bool dist_graph = [] {
+    const char* e = std::getenv("YY_DIST_GRAPH");
+    return e && e[0] == '1';
+  }();
   const bool graph = ctx->use_graph && ctx->st != nullptr && !ctx->prof_on &&
-                     ((cs.size() == 1 && ctx->mode == 0) || (ctx->mode == 1 && ctx->schwarz == 0));
+                     ((cs.size() == 1 && ctx->mode == 0) || (ctx->mode == 1 && ctx->schwarz == 0) ||
+                      (dist_graph && ctx->mode == 2 && ctx->schwarz == 0));
   cudaGraphExec_t gexec = nullptr;
   std::vector<long long> glaunches(cs.size(), 0);
   if (graph && ctx->use_graph == 2 && cs.size() == 1 && ctx->mode == 0) {
@@ -1447,10 +1480,16 @@ static yy_status set_terms(yy_ctx* ctx, int32_t patch, int32_t nterms, const int
       double*& slot = wall ? ctx->wterm[patch][m][f] : ctx->sterm[patch][m][f];
       if (!src[f]) { slot = nullptr; continue; }
       const long long sz = wall ? 2 * wsize(g, WKIND[f]) : psize(g, WKIND[f]);
-      double* d = nullptr;
-      TRY(dalloc(ctx, &d, sz));
-      CK(cudaMemset(d, 0, sz * sizeof(double)));
-      if (wall) CK(cudaMemcpy(d, src[f], sz * sizeof(double), cudaMemcpyHostToDevice));
+      // a slot's size depends only on (wall|source, field): re-setting terms reuses
+      // the buffer allocated by the first call instead of allocating again
+      double*& keep = wall ? ctx->wterm_buf[patch][m][f] : ctx->sterm_buf[patch][m][f];
+      if (!keep) TRY(dalloc(ctx, &keep, sz));
+      double* d = keep;
+      CK(cudaMemsetAsync(d, 0, sz * sizeof(double), ctx->st));
+      if (wall) {
+        CK(cudaMemcpyAsync(d, src[f], sz * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+      }
       else TRY(copy_window(ctx, WKIND[f], d, const_cast<double*>(src[f]), true, false));
       slot = d;
     }
@@ -1466,6 +1505,25 @@ yy_status yy_set_wall(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t*
 
 yy_status yy_set_source(yy_ctx* ctx, int32_t patch, int32_t nterms, const int32_t* timefn, const yy_fields* terms) {
   return set_terms(ctx, patch, nterms, timefn, terms, false);
+}
+
+yy_status yy_energy(yy_ctx* ctx, double* out3) {
+  if (!ctx || !out3) return YY_EINVAL;
+  if (ctx->dead) return fail(ctx, YY_ESTATE, "context unusable after a CUDA error");
+  if (ctx->nslab > 1) return fail(ctx, YY_EINVAL, "yy_energy needs whole patches (no radial slabs)");
+  const Geo& g = ctx->g;
+  const long long zw = 2 * wsize(g, KC) * g.npatch, nb = energy_blocks(g);
+  if (!ctx->energy_buf) {
+    TRY(dalloc(ctx, &ctx->energy_buf, zw + 3 * nb + 3));
+    CK(cudaMemsetAsync(ctx->energy_buf, 0, zw * sizeof(double), ctx->st));
+  }
+  launch_energy(g, ctx->n[FT], ctx->m[FT], ctx->energy_buf, ctx->energy_buf + zw, ctx->energy_buf + zw + 3 * nb,
+                ctx->st);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out3, ctx->energy_buf + zw + 3 * nb, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return YY_OK;
 }
 
 yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
@@ -1488,7 +1546,8 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       ctx->fixed_iters = (int)v;
       return YY_OK;
     case YY_SCHWARZ:
-      if (v != 0 && v != 1) return fail(ctx, YY_EINVAL, "schwarz must be 0 (additive) or 1 (multiplicative)");
+      if (v != 0 && v != 1 && v != 2)
+        return fail(ctx, YY_EINVAL, "schwarz must be 0 (additive), 1 (multiplicative) or 2 (none: single domains)");
       if (v == 1 && ctx->g.npatch == 2)
         return fail(ctx, YY_EINVAL, "multiplicative Schwarz needs one patch per context (yy_create_pair/_slabs/_dist)");
       ctx->schwarz = (int)v;
@@ -1507,6 +1566,25 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       if (ctx->mode == 1)
         for (yy_ctx* c : ctx->group) if (c) c->heat_only = ctx->heat_only;
       return YY_OK;
+    case YY_ADVECTION: {
+      if (v != 0 && v != 1) return fail(ctx, YY_EINVAL, "advection must be 0 (in the split factors) or 1 (IMEX)");
+      auto set = [&](yy_ctx* c) -> yy_status {
+        c->imex = v != 0;
+        if (c->imex && !c->zero) {
+          long long mx = 0;
+          for (int K = 0; K < 4; ++K) mx = std::max(mx, c->g.npatch * psize(c->g, K));
+          TRY(dalloc(c, &c->zero, mx));
+          CK(cudaMemset(c->zero, 0, mx * sizeof(double)));
+        }
+        for (int K = 0; K < 4; ++K)
+          for (int ax = 0; ax < 3; ++ax) c->g.adv[K][ax] = c->imex ? c->zero : c->adv[K][ax];
+        return YY_OK;
+      };
+      TRY(set(ctx));
+      if (ctx->mode == 1)
+        for (yy_ctx* c : ctx->group) if (c && c != ctx) TRY(set(c));
+      return YY_OK;
+    }
     case YY_INTERP_ORDER:
       if (v != 4) return fail(ctx, YY_EINVAL, "interpolation order: only 4 (4x4 Lagrange, RD4) is built");
       return YY_OK;

@@ -31,6 +31,7 @@ struct StaticArgs {
   double gsrc[2][MAXSRC];
   int nsrc[2];
   double* G[2];
+  int imex;                  // the -1/2 L_split term without transport terms (YY_ADVECTION = 1)
 };
 
 struct ResidArgs {
@@ -161,6 +162,10 @@ int launch_pres(const Geo& g, int s, const PresArgs& a, cudaStream_t st);
 void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, cudaStream_t st);
 // rho = max over the 2 NSLOT sums -> out[0], NaN flag -> out[1]
 void launch_reduce_final(double* out, cudaStream_t st);
+// Theorem 1 diagnostic (yy_energy): out[3] = (1/2 (-L T, T)_w, 1/4 ||dT||^2_D, ||dT||^2_w)
+int energy_blocks(const Geo& g);
+void launch_energy(const Geo& g, const double* Tn, const double* Tm, const double* zw, double* part, double* out,
+                   cudaStream_t st);
 // device-side Schwarz loop: ctl = {iterations, rho, NaN flag}; sets the WHILE
 // node's condition h (continue: no NaN, k < kmax, fixed or rho >= tol)
 void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double* ctl, double tol, int kmax,

@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
       }
     }
     const double Lf = applyL<Q, false>(g, A, i, j, k, S);
-    const double Ls = applyL<Q, true>(g, A, i, j, k, D);
+    // IMEX: the split operator without its transport terms (a* = 0)
+    const double Ls = a.imex ? applyL<Q, true, RX_GIVEN>(g, A, i, j, k, D) : applyL<Q, true>(g, A, i, j, k, D);
     a.G[s][po + node] = g.tau * (Lf - 0.5 * Ls + E);
   }
 }
@@ -247,6 +248,73 @@ __global__ void __launch_bounds__(128) k_pres(Geo g, PresArgs a) {
   const double t = block_sum<128>(w);
   if (threadIdx.x == 0)
     a.part[(long long)patch * a.maxb + ((B.z % nz) * gridDim.y + B.y) * gridDim.x + B.x] = t;
+}
+
+// ---------------------------------------------------------------------------------
+// Theorem 1 diagnostic (eq:Stability; oracle/energy.py): per block the
+// omega-weighted sums of  (-L T^n) T^n,  (-(Lh - L)_{th+ph} d) d  and  d d,
+// d = T^n - T^{n-1}, over the solved cell centres, with the T rows of coef<>
+// (u = 0: pure diffusion) and homogeneous wall data (the theorem's setting).
+// One thread per (j, k) column walking r; block = 128 k.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_energy(Geo g, const double* __restrict__ Tn, const double* __restrict__ Tm,
+                                                const double* __restrict__ zw, double* __restrict__ part) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1, j = blockIdx.y + 1, patch = blockIdx.z;
+  const Astar A{};
+  double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+  if (k <= g.np - 2 && j <= g.nt - 2) {
+    const double* tn = Tn + patch * psize(g, KC);
+    const double* tm = Tm + patch * psize(g, KC);
+    for (int i = g.ilo_c; i <= g.ihi_c; ++i) {
+      const Star a = load_star<KC>(g, tn, zw, i, j, k);
+      const Star b = load_star<KC>(g, tm, zw, i, j, k);
+      const Star d = star_lin(a, 1.0, b, -1.0);
+      double am, a0, ap, hm, h0, hp;
+      coef<QT, 0, false, false>(g, A, i, j, k, am, a0, ap);
+      double LT = am * a.xm + a0 * a.c + ap * a.xp;
+      coef<QT, 1, false, false>(g, A, i, j, k, am, a0, ap);
+      coef<QT, 1, true, false>(g, A, i, j, k, hm, h0, hp);
+      LT += am * a.ym + a0 * a.c + ap * a.yp;
+      double DL = (hm - am) * d.ym + (h0 - a0) * d.c + (hp - ap) * d.yp;
+      coef<QT, 2, false, false>(g, A, i, j, k, am, a0, ap);
+      coef<QT, 2, true, false>(g, A, i, j, k, hm, h0, hp);
+      LT += am * a.zm + a0 * a.c + ap * a.zp;
+      DL += (hm - am) * d.zm + (h0 - a0) * d.c + (hp - ap) * d.zp;
+      const double w = omega(g, __ldg(g.rc + i), __ldg(g.sc + j));
+      e0 += w * (-LT) * a.c;
+      e1 += w * (-DL) * d.c;
+      e2 += w * d.c * d.c;
+    }
+  }
+  // block_sum's shared scratch is reused: a barrier between the three sums
+  const double s0 = block_sum<128>(e0);
+  __syncthreads();
+  const double s1 = block_sum<128>(e1);
+  __syncthreads();
+  const double s2 = block_sum<128>(e2);
+  if (threadIdx.x == 0) {
+    double* o = part + 3LL * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    o[0] = s0;
+    o[1] = s1;
+    o[2] = s2;
+  }
+}
+
+// fixed-order sum of the k_energy partials: out = (1/2 e0, 1/4 e1, e2)
+__global__ void __launch_bounds__(128) k_energy_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < nb; b += 128)
+    for (int c = 0; c < 3; ++c) v[c] += part[3LL * b + c];
+  const double s0 = block_sum<128>(v[0]);
+  __syncthreads();
+  const double s1 = block_sum<128>(v[1]);
+  __syncthreads();
+  const double s2 = block_sum<128>(v[2]);
+  if (threadIdx.x == 0) {
+    out[0] = 0.5 * s0;
+    out[1] = 0.25 * s1;
+    out[2] = s2;
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -647,6 +715,14 @@ void launch_reduce_slots(const double* part, const ReduceArgs& a, double* out, c
 }
 
 void launch_reduce_final(double* out, cudaStream_t st) { k_reduce_final<<<1, 32, 0, st>>>(out); }
+
+int energy_blocks(const Geo& g) { return ((g.np - 2 + 127) / 128) * (g.nt - 2) * g.npatch; }
+void launch_energy(const Geo& g, const double* Tn, const double* Tm, const double* zw, double* part, double* out,
+                   cudaStream_t st) {
+  const dim3 grid((g.np - 2 + 127) / 128, g.nt - 2, g.npatch);
+  k_energy<<<grid, 128, 0, st>>>(g, Tn, Tm, zw, part);
+  k_energy_final<<<1, 128, 0, st>>>(part, energy_blocks(g), out);
+}
 
 // Device-side Schwarz loop control (the body's last node when the loop runs as a
 // conditional WHILE graph node): count the iteration, record rho and the NaN flag

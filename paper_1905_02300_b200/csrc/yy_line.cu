@@ -42,6 +42,9 @@
 #ifndef YY_LINE_MINB
 #define YY_LINE_MINB 0   // >0: force this __launch_bounds__ min blocks per SM (tuning)
 #endif
+#ifndef YY_RT_MENU
+#define YY_RT_MENU 0     // r / theta chunkings for n <= 128: 0 (16,6)/(16,8); 1 (8,12)/(8,16); 2 (32,3)/(32,4)
+#endif
 
 namespace yy {
 
@@ -724,6 +727,13 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
     if (n <= 16) YY_L(4, 4);
     if (n <= 32) YY_L(4, 8);
     if (n <= 64) YY_L(8, 8);
+#if YY_RT_MENU == 1
+    if (n <= 96) YY_L(8, 12);
+    if (n <= 128) YY_L(8, 16);
+#elif YY_RT_MENU == 2
+    if (n <= 96) YY_L(32, 3);
+    if (n <= 128) YY_L(32, 4);
+#endif
     if (n <= 96) YY_L(16, 6);
     if (n <= 128) YY_L(16, 8);
     if (n <= 256) YY_L(16, 16);

@@ -29,38 +29,38 @@ constexpr int MAXS = 8;   // slabs per patch
 __global__ void k_slab_solve(SlabArgs a) {
   const int line = blockIdx.x * blockDim.x + threadIdx.x;
   if (line >= a.nlines) return;
-  const int S = a.nslab, N = 2 * S;
-  double M[2 * MAXS][2 * MAXS + 1];
-  for (int r = 0; r < N; ++r)
-    for (int c = 0; c <= N; ++c) M[r][c] = 0.0;
+  const int S = a.nslab;
+  // The 2S boundary unknowns in the order (.., b_{s-1}, a_s, b_s, a_{s+1}, ..) form a
+  // banded system (row a_s: b_{s-1}, a_s, a_{s+1}; row b_s: b_{s-1}, b_s, a_{s+1}):
+  // one forward sweep keeps b_{s-1} = be + ga a_s and gives a_s = p_s + q_s a_{s+1},
+  // the backward sweep from a_S = 0 recovers every a_s (O(S) work, no pivoting: the
+  // couplings are responses of diagonally dominant lines, |.| < 1; the same
+  // elimination as the boundary system of the multi-warp phi lines, yy_line.cu)
+  double p[MAXS], q[MAXS], bb[MAXS], gg[MAXS];
+  double be = 0.0, ga = 0.0;                 // b_{-1} = 0: no slab below the first
   for (int s = 0; s < S; ++s) {
     const double* f = a.IFall + ((long long)s * a.nlines + line) * 6;
-    for (int h = 0; h < 2; ++h) {          // h = 0: first row (a_s), 1: last row (b_s)
-      const int r = 2 * s + h;
-      M[r][r] = 1.0;
-      if (s > 0) M[r][2 * s - 1] -= f[3 * h + 1];        // b_{s-1}
-      if (s < S - 1) M[r][2 * s + 2] -= f[3 * h + 2];    // a_{s+1}
-      M[r][N] = f[3 * h + 0];
+    const double d = 1.0 / (1.0 - f[1] * ga);
+    p[s] = (f[0] + f[1] * be) * d;
+    q[s] = f[2] * d;
+    bb[s] = be;
+    gg[s] = ga;
+    be = f[3] + f[4] * (be + ga * p[s]);
+    ga = f[4] * ga * q[s] + f[5];
+  }
+  const int me = a.slab;
+  double an = 0.0;                           // a_{s+1}; a_S = 0: no slab above the last
+  double xlo = 0.0, xhi = 0.0;
+  for (int s = S - 1; s >= 0; --s) {
+    const double as = p[s] + q[s] * an;
+    if (s == me) {
+      xlo = s > 0 ? bb[s] + gg[s] * as : 0.0;   // b_{s-1}
+      xhi = s < S - 1 ? an : 0.0;               // a_{s+1}
     }
+    an = as;
   }
-  // Gaussian elimination (the couplings are responses of diagonally dominant lines: |.| < 1)
-  for (int p = 0; p < N; ++p) {
-    const double ip = 1.0 / M[p][p];
-    for (int r = p + 1; r < N; ++r) {
-      const double m = M[r][p] * ip;
-      if (m != 0.0)
-        for (int c = p; c <= N; ++c) M[r][c] -= m * M[p][c];
-    }
-  }
-  double z[2 * MAXS];
-  for (int r = N - 1; r >= 0; --r) {
-    double v = M[r][N];
-    for (int c = r + 1; c < N; ++c) v -= M[r][c] * z[c];
-    z[r] = v / M[r][r];
-  }
-  const int s = a.slab;
-  a.LH[2LL * line + 0] = s > 0 ? z[2 * s - 1] : 0.0;
-  a.LH[2LL * line + 1] = s < S - 1 ? z[2 * s + 2] : 0.0;
+  a.LH[2LL * line + 0] = xlo;
+  a.LH[2LL * line + 1] = xhi;
 }
 
 // grid: x -> k (128 per block), y -> j, z -> owned row

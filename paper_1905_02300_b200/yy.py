@@ -17,12 +17,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 YY_OK, YY_ENOCONV = 0, 4
 YY_CHI, YY_MAX_ITERS, YY_FIXED_ITERS, YY_PROFILE, YY_SCHWARZ, YY_HEAT_ONLY, YY_FLUX_FIX = 1, 2, 3, 4, 5, 6, 7
 YY_INTERP_ORDER = 8
+YY_ADVECTION = 9
 TF_ONE, TF_COS, TF_SIN, TF_COS2 = 0, 1, 2, 3
+SCHWARZ = {"additive": 0, "multiplicative": 1, "none": 2}
 
 EXPORTS = ("yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
            "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_time",
            "yy_last_error", "yy_destroy", "yy_debug_get", "yy_line_solve", "yy_line_prepare", "yy_launch_count",
-           "yy_profile_report", "yy_set_allocator")
+           "yy_profile_report", "yy_set_allocator", "yy_energy")
 
 
 class YYError(RuntimeError):
@@ -91,9 +93,10 @@ def load_library():
     L.yy_create_dist.argtypes = [POINTER(yy_grid), c_double, c_double, c_double, c_double, c_double,
                                  c_int32, c_int32, c_void_p, c_int32, POINTER(ctx)]
     L.yy_nccl_unique_id.argtypes = [c_void_p]
+    L.yy_energy.argtypes = [ctx, _DP]
     for name in ("yy_create_pair", "yy_create_slabs", "yy_create_dist", "yy_nccl_unique_id", "yy_create", "yy_set_fields", "yy_get_fields", "yy_set_wall", "yy_set_source",
                  "yy_set_param", "yy_set_stream", "yy_step", "yy_get_stats", "yy_debug_get", "yy_line_solve", "yy_line_prepare",
-                 "yy_profile_report", "yy_set_allocator"):
+                 "yy_profile_report", "yy_set_allocator", "yy_energy"):
         getattr(L, name).restype = c_int32
     _lib = L
     return L
@@ -108,7 +111,7 @@ class Shell:
 
     def __init__(self, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3,
                  chi=None, max_iters=None, fixed_iters=None, stream=None, heat_only=False, flux_fix_eps=None,
-                 _handle=None, _patches=(0, 1)):
+                 schwarz=None, advection=None, _handle=None, _patches=(0, 1)):
         self.L = load_library()
         self.nr, self.nt, self.np_ = nr, ntheta, nphi
         self.patches = tuple(_patches)        # patches this context holds
@@ -132,6 +135,10 @@ class Shell:
             self.set_param(YY_HEAT_ONLY, 1)
         if flux_fix_eps is not None:
             self.set_param(YY_FLUX_FIX, flux_fix_eps)
+        if schwarz is not None:
+            self.set_param(YY_SCHWARZ, SCHWARZ[schwarz])
+        if advection is not None:
+            self.set_param(YY_ADVECTION, {"split": 0, "imex": 1}[advection])
 
     @classmethod
     def pair(cls, nr, ntheta, nphi, R1=1.0, R2=2.0, Pr=1.0, Ra=0.0, dt=1e-3, **kw):
@@ -178,7 +185,10 @@ class Shell:
         sh._configure(**kw)
         return sh
 
-    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None, schwarz=None, flux_fix_eps=None):
+    def _configure(self, chi=None, max_iters=None, fixed_iters=None, stream=None, schwarz=None, flux_fix_eps=None,
+                   advection=None):
+        if advection is not None:
+            self.set_param(YY_ADVECTION, {"split": 0, "imex": 1}[advection])
         if chi is not None:
             self.set_param(YY_CHI, chi)
         if max_iters is not None:
@@ -188,7 +198,7 @@ class Shell:
         if stream is not None:
             self.set_stream(stream)
         if schwarz is not None:
-            self.set_param(YY_SCHWARZ, {"additive": 0, "multiplicative": 1}[schwarz])
+            self.set_param(YY_SCHWARZ, SCHWARZ[schwarz])
         if flux_fix_eps is not None:
             self.set_param(YY_FLUX_FIX, flux_fix_eps)
 
@@ -297,6 +307,12 @@ class Shell:
             name, n, ms = line.split()
             out[name] = (int(n), float(ms))
         return out
+
+    def energy(self):
+        """yy_energy: (1/2 (-L T, T)_w, 1/4 ||dT||^2_D, ||dT||^2_w) of eq:Stability."""
+        out = (c_double * 3)()
+        self._check(self.L.yy_energy(self.h, out), "yy_energy")
+        return tuple(out)
 
     def debug_get(self, name, patch):
         kind = {"astar_r": "ur", "astar_t": "ut", "astar_p": "up", "G_T": "T"}.get(name)

@@ -28,3 +28,21 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the per-field parity metric of every GPU parity test (BASELINE.md
+    §2) next to the run's other GPU evidence when gpurun_out/ exists."""
+    try:
+        import json
+        from tests import test_gpu_parity as tp   # noqa: F401
+    except Exception:
+        try:
+            import json
+            import test_gpu_parity as tp          # noqa: F401
+        except Exception:
+            return
+    out = os.path.join(ROOT, "gpurun_out")
+    if tp.PER_FIELD and os.path.isdir(out):
+        with open(os.path.join(out, "parity_per_field.json"), "w") as fh:
+            json.dump(tp.PER_FIELD, fh, indent=1)

@@ -25,20 +25,30 @@ def _shell(cfg, **kw):
     return Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, **kw)
 
 
-@pytest.mark.parametrize("name,steps", [("C2", 1), ("C3", 1), ("C5", 1), ("C3", 3), ("C2", 5),
-                                        ("C2", 100)])
-def test_full_size_steps_match_oracle_golden(name, steps):
+GOLDEN_CASES = [("C2", 1, ""), ("C3", 1, ""), ("C5", 1, ""), ("C3", 3, ""), ("C2", 5, ""), ("C2", 100, ""),
+                # the BASELINE workloads' chi = 16 (DESIGN.md RD-E4), as bench.py runs them
+                ("C2", 1, "_chi16"), ("C2", 5, "_chi16"), ("C2", 100, "_chi16"), ("C2", 200, "_chi16"),
+                ("C3", 1, "_chi16"), ("C3", 3, "_chi16"), ("C3", 5, "_chi16"), ("C3", 10, "_chi16"),
+                ("C5", 1, "_chi16"), ("C5", 3, "_chi16")]
+
+
+@pytest.mark.parametrize("name,steps,tag", GOLDEN_CASES)
+def test_full_size_steps_match_oracle_golden(name, steps, tag):
     """Full BASELINE size, the bench launch configuration: `steps` steps from the
     workload's initial state; every step's Schwarz count equal; sampled nodes
     within 1e-11 per step taken (errors of independent steps add; 100 steps:
     the BASELINE 1e-9 bar)."""
-    path = os.path.join(GOLD, f"{name.lower()}_step{steps}.json")
+    path = os.path.join(GOLD, f"{name.lower()}{tag}_step{steps}.json")
     if not os.path.exists(path):
         pytest.skip(f"{path} not generated yet (tools/make_golden.py --steps {steps} {name})")
     gold = json.load(open(path))
     cfg = W.config(name)
     assert gold["grid"] == [cfg.nr, cfg.nth, cfg.nph]
-    sh = _shell(cfg)
+    # the launch configuration bench.py times: a user stream (device-side Schwarz
+    # loop in one CUDA graph) and the golden's chi (round-1 files: chi = 1)
+    import torch
+    st = torch.cuda.Stream()
+    sh = _shell(cfg, chi=gold.get("chi", 1.0), stream=st.cuda_stream)
     sh.load_workload(W.make_workload(cfg))
     sh.step(steps, cfg.tol)
     ks = [k for k, _ in sh.stats()[-steps:]]

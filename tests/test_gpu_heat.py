@@ -58,3 +58,42 @@ def test_heat_douglas_unconditionally_stable(tau):
         assert np.isfinite(m)
         worst = max(worst, m)
     assert worst <= 10 * m0, (tau, worst / m0)
+
+
+@pytest.mark.parametrize("tau", [0.1, 1.0, 10.0, 100.0])
+def test_theorem1_energy_parity_and_monotone(tau):
+    """Theorem 1 proper (eq:Stability): single domains (YY_SCHWARZ = 2, no
+    exchange), homogeneous Dirichlet data on every side (zero fringe and walls),
+    one factored solve per step (eq:HeatDouglas).  The left side of eq:Stability
+    from yy_energy is non-increasing step by step, and equals the oracle's
+    (oracle/energy.py) step by step within 1e-11 relative (SPEC criterion 4 grid
+    and tau values)."""
+    from oracle.energy import stability_terms
+    from paper_1905_02300_b200 import Shell
+    nr, nt, npp = 8, 24, 48
+    rng = np.random.default_rng(4)
+    sh = Shell(nr, nt, npp, 1.0, 2.0, 1.0, 0.0, tau, heat_only=True, fixed_iters=1, schwarz="none")
+    o = Oracle(nr, nt, npp, 1.0, 2.0, 1.0, 0.0, tau, fixed_iters=1, schwarz="none")
+    for p in range(2):
+        T = np.zeros((nr, nt, npp))
+        T[:, 1:-1, 1:-1] = rng.standard_normal((nr, nt - 2, npp - 2))
+        sh.set_fields(p, 0, 0, T=T)
+        sh.set_fields(p, 1, 0, T=T)
+        o.set_fields(p, 0, 0, {"T": T})
+        o.set_fields(p, 1, 0, {"T": T})
+    Sg, So, acc_g, acc_o = [], [], 0.0, 0.0
+    for n in range(13):
+        if n:
+            sh.step(1, 1e-10)
+            o.step(1, 1e-10)
+        eg = sh.energy()
+        eo = [sum(x) for x in zip(*(stability_terms(o, p) for p in range(2)))]
+        for a, b in zip(eg, eo):
+            assert abs(a - b) <= 1e-11 * max(abs(eo[0]), 1e-300), (n, eg, eo)
+        acc_g += eg[2] / tau if n else 0.0
+        acc_o += eo[2] / tau if n else 0.0
+        Sg.append(acc_g + eg[0] + eg[1])
+        So.append(acc_o + eo[0] + eo[1])
+    dS = np.diff(Sg)
+    assert np.all(dS < 0) and np.all(dS <= 1e-12 * Sg[0]), dS / Sg[0]
+    assert np.max(np.abs(np.array(Sg) - np.array(So))) <= 1e-11 * So[0]

@@ -60,6 +60,11 @@ class Config:
     steps: int = 1
     tol: float = 1e-10
     problem: str = "manufactured"      # manufactured | landau | convection
+    # artificial-compressibility chi (eq:ac1).  The paper asks chi = O(1); on the
+    # R2/R1 = 2 shell the fixed point of the step is stable only for chi >= beta =
+    # R2^2 / (R1^2 sin^2 theta_1) (DESIGN.md RD-E4: Fourier model, oracle, C2 drift
+    # on the GPU), beta = 8.3 (C5) ... 16 (C1): every BASELINE workload takes 16.
+    chi: float = 16.0
     extra: dict = field(default_factory=dict)
 
     @property
