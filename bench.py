@@ -10,8 +10,9 @@ Prints ONE JSON line (rank 0).  Metric: cell-updates/s = 2 patches x cells
 per patch x steps / device time (BASELINE.json metric); inputs larger than L2
 (the C3 working set is ~2.8 GB), so no flush is needed between steps.
 
---impl reference runs the CPU oracle (oracle/, plain numpy fp64) on a bounded
-sample of the same workload (full time steps on a 1/64-cell copy of it).
+--impl reference runs the CPU oracle (oracle/, plain numpy fp64) on the same
+workload at full size, bounded: the static part of one step and a few Schwarz
+iterations, each timed, extrapolated to the oracle's own Schwarz count.
 """
 from __future__ import annotations
 
@@ -31,7 +32,6 @@ sys.path.insert(0, ROOT)
 METRIC = "full time steps: cell-updates/s and % of HBM roofline at 1/2/4/8 B200"
 UNIT = "cell-updates/s"
 HBM_NOMINAL_GBS = 8000.0          # BASELINE.json roofline denominator (8 TB/s)
-SAMPLE_DIV = {"C1": 1, "C2": 2, "C3": 2, "C5": 2}   # CPU sample grid = workload grid / d per axis (~10 s of oracle work per step)
 
 
 def measured_peak():
@@ -135,8 +135,8 @@ def m1_bytes(name, cfg, nsrc):
         return 8 * P * kind_nodes(cfg, QK[q]) * (reads + writes)
     if name.startswith("pres_"):
         return 8 * P * kind_nodes(cfg, "C") * (8 + (2 if name.endswith("2") else 0) + 1)
-    if name == "astar":
-        return 8 * P * kind_nodes(cfg, "R") * 3
+    if name == "astar":      # one launch: the three components of a* = 1.5 u2^n - 0.5 u2^{n-1}
+        return 8 * P * 3 * sum(kind_nodes(cfg, k) for k in ("R", "TH", "PH"))
     return 0
 
 
@@ -161,20 +161,32 @@ def step_model_bytes(cfg, K, forced):
 # ---------------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------------
-def oracle_sample_step(cfg_name):
-    """One complete time step of the workload's physics on a 1/d^3-cell copy of
-    its grid, by the plain numpy oracle.  Returns (cells, seconds, K)."""
+def oracle_full_grid(cfg_name, n_iters):
+    """The plain numpy oracle on the workload's FULL grid: the static part of one
+    time step (a*, G) and its first n_iters Schwarz iterations, each timed (the
+    oracle's own timing hooks).  A full step costs t_static + K t_iter, so the
+    rate at any Schwarz count K follows without running all K iterations.
+    Returns (cells, t_static, [t_iter ...])."""
     import workloads as W
     from oracle.scheme import Oracle
-    full = W.config(cfg_name)
-    d = SAMPLE_DIV[cfg_name]
-    c = W.small(cfg_name, full.nr // d, full.nth // d, full.nph // d)
-    o = Oracle(c.nr, c.nth, c.nph, c.R1, c.R2, c.Pr, c.Ra, c.dt, chi=c.chi)
+    c = W.config(cfg_name)
+    o = Oracle(c.nr, c.nth, c.nph, c.R1, c.R2, c.Pr, c.Ra, c.dt, chi=c.chi, fixed_iters=n_iters)
     o.load_workload(W.make_workload(c))
-    t0 = time.perf_counter()
     o.step(1, c.tol)
-    dt = time.perf_counter() - t0
-    return 2 * c.cells, dt, o.stats[-1][0], (c.nr, c.nth, c.nph)
+    return 2 * c.cells, o.timing["static"], list(o.timing["iters"])
+
+
+def oracle_reference_K(cfg_name):
+    """The oracle's own Schwarz count for the first step of the workload at full
+    size, from the committed golden (tools/make_golden.py, oracle only), or None."""
+    import workloads as W
+    chi = W.config(cfg_name).chi
+    tag = "" if chi == 1.0 else f"_chi{chi:g}"
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", f"{cfg_name.lower()}{tag}_step1.json")) as f:
+            return int(json.load(f)["schwarz_iters"])
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def cpu_cores_used():
@@ -236,23 +248,26 @@ def emit(obj):
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle as it stands on the workload's full grid.
+    One bench step = one Schwarz iteration of the full-grid step (the static part
+    is timed once before); the line's value is the full-step rate at the oracle's
+    own Schwarz count K (golden of the first step), cells / (t_static + K t_iter)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    steps = []
-    for i in range(args.warmup + args.steps):
-        cells, sec, K, grid = oracle_sample_step(args.workload)
-        if i >= args.warmup:
-            steps.append((cells, sec, K))
-    tot_cells = sum(s[0] for s in steps)
-    tot_sec = sum(s[1] for s in steps)
-    v = tot_cells / tot_sec
-    sample = (f"{args.workload} physics on a {grid[0]}x{grid[1]}x{grid[2]} per-patch grid (1/{SAMPLE_DIV[args.workload] ** 3} "
-              f"of the cells), one full time step per bench step, mean Schwarz K={statistics.mean(s[2] for s in steps):.1f}")
+    cells, t_static, iters = oracle_full_grid(args.workload, args.warmup + args.steps)
+    timed = iters[args.warmup:]
+    t_iter = sum(timed) / len(timed)
+    K = oracle_reference_K(args.workload) or len(iters)
+    t_step = t_static + K * t_iter
+    v = cells / t_step
+    sample = (f"{args.workload} at full size (2 x {cells // 2} cells): the static part of the first time step "
+              f"({t_static:.1f} s) and {args.warmup} untimed + {args.steps} timed Schwarz iterations "
+              f"({t_iter:.1f} s each), extrapolated to the oracle's own K = {K} of that step")
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": max(world, args.gpus),
-          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_sec / len(steps),
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step,
           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-          "data": "synthetic", "config": {"workload": args.workload, "sample": sample},
+          "data": "synthetic", "config": {"workload": args.workload, "sample": sample, "schwarz_iters": K},
           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle", "sample": sample},
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     return 0
@@ -278,7 +293,7 @@ def run_yy(args):
     forced = nsrc > 0
     stream = torch.cuda.Stream()
     sh = Shell(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, stream=stream.cuda_stream,
-               chi=cfg.chi, **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
+               chi=cfg.chi, advection=args.advection, **({"fixed_iters": args.fixed_iters} if args.fixed_iters else {}))
     sh.load_workload(wl)
     W_ = max(3, args.warmup)
     for _ in range(W_):
@@ -374,17 +389,21 @@ def run_yy(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        c_cells, c_sec, c_K, grid = oracle_sample_step(args.workload)
+        c_cells, t_static, t_iters = oracle_full_grid(args.workload, 1)
+        K_mean = sum(Ks) / len(Ks)
+        c_sec = t_static + K_mean * t_iters[0]
         cpu = {"value": c_cells / c_sec, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
-               "sample": f"one full time step of {args.workload} physics on a {grid[0]}x{grid[1]}x{grid[2]} "
-                         f"per-patch grid (1/{SAMPLE_DIV[args.workload] ** 3} of the cells), Schwarz K={c_K}, {c_sec:.1f} s"}
+               "sample": f"{args.workload} at full size: the static part ({t_static:.1f} s) and the first "
+                         f"Schwarz iteration ({t_iters[0]:.1f} s) of one full-grid time step by the plain numpy "
+                         f"oracle, extrapolated to the GPU steps' mean K = {K_mean:.1f}",
+               "per_schwarz_iteration": {"value": c_cells / t_iters[0], "unit": "cell-iterations/s"}}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": W_,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "grid_per_patch": [cfg.nr, cfg.nth, cfg.nph], "patches": 2,
-                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra, "chi": cfg.chi,
+                   "dt": cfg.dt, "Pr": cfg.Pr, "Ra": cfg.Ra, "chi": cfg.chi, "advection": args.advection,
                    "schwarz_tol": cfg.tol if not args.fixed_iters else f"fixed K = {args.fixed_iters}",
                    "schwarz_iters_per_step": Ks, "l2_flush": "inputs larger than L2 (working set ~37 fp64 fields)",
                    "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
@@ -488,6 +507,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fixed-iters", type=int, default=0,
                     help="Schwarz iterations per step fixed (the paper's scaling protocol, C5: 10); 0 = to tolerance")
+    ap.add_argument("--advection", default="split", choices=("split", "imex"),
+                    help="transport terms in the split factors (the paper's scheme) or IMEX (SURVEY NEXT-3)")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)   # CPU test of the rank launch
     args = ap.parse_args()
     if args.gpus < 1:

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import copy
 import math
+import time
 
 import numpy as np
 
@@ -288,7 +289,12 @@ class Oracle:
         tau = prm.dt
         t = self.t
         self._cc = {}
+        # wall-clock of the static part and of every iteration (instrumentation
+        # for bench.py's CPU baseline; no effect on the arithmetic)
+        t0 = time.perf_counter()
         stat = [self.static(p, t) for p in range(2)]
+        self.timing = {"static": time.perf_counter() - t0, "iters": []}
+        t_it = time.perf_counter()
         cur = [copy.deepcopy(self.state[p]["n"]) for p in range(2)]
         wnew = [{name: self.wall(p, name, t + tau) for name in ("T", "ur", "ut", "up")} for p in range(2)]
         wdiff = [{name: wnew[p][name] - self.wall(p, name, t) for name in ("T", "ut", "up")} for p in range(2)]
@@ -352,6 +358,9 @@ class Oracle:
             rho = 0.0
             for p in range(2):
                 rho = max(rho, self._iterate_patch(p, cur[p], stat[p], wdiff[p]))
+            now = time.perf_counter()
+            self.timing["iters"].append(now - t_it)
+            t_it = now
             if not self.fixed_iters and rho < tol:
                 break
         for p in range(2):

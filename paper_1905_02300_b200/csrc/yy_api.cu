@@ -65,6 +65,19 @@ struct yy_ctx {
                                // 2 none (single domains, Theorem 1)
   double* energy_buf = nullptr;   // yy_energy: zero wall + block partials + result
   bool imex = false;           // YY_ADVECTION = 1: transport terms explicit only
+  // instantiated device-loop graphs (one step's Schwarz loop, YY_GRAPH=2), keyed by
+  // everything the captured launches bake in: the level pointers rotate through a
+  // short cycle (3 for T/u, 2 for p), so a run replays a handful of executables
+  // instead of capturing and instantiating one per step; cleared by set_param /
+  // set_stream
+  struct LoopGraph {
+    std::vector<const void*> key;
+    double tol;
+    int rev_in, rev_out;
+    long long per_iter;
+    cudaGraphExec_t exec;
+  };
+  std::vector<LoopGraph> loop_graphs;
   double* zero = nullptr;      // IMEX: zero a* / row-weight / reaction arrays of the split rows
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
@@ -176,6 +189,11 @@ yy_status dalloc(yy_ctx* ctx, T** p, size_t count) {
     yy_status s_ = (x);             \
     if (s_ != YY_OK) return s_;     \
   } while (0)
+
+void clear_loop_graphs(yy_ctx* ctx) {
+  for (auto& lg : ctx->loop_graphs) cudaGraphExecDestroy(lg.exec);
+  ctx->loop_graphs.clear();
+}
 
 // ---- instrumentation ----------------------------------------------------------------
 cudaEvent_t ev_get(yy_ctx* ctx) {
@@ -429,21 +447,25 @@ yy_status check_args(yy_ctx* ctx, int32_t patch, int32_t level, int32_t system) 
 }
 
 // ---- one time step ------------------------------------------------
-yy_status eval_walls(yy_ctx* ctx, int L, double t) {
+// the wall data of time level L (0: t_{n-1}, 1: t_n, 2: t_{n+1}) of every field and
+// patch, appended to one batch of linear combinations of the time-basis terms
+yy_status eval_walls(yy_ctx* ctx, int L, double t, LinBatch& b) {
   const Geo& g = ctx->g;
   for (int f = 0; f < NW; ++f) {
     const long long ws = 2 * wsize(g, WKIND[f]);   // inner + outer wall of one patch
     for (int p = 0; p < g.npatch; ++p) {
-      LinIn in{};
+      if (b.njobs >= MAXLIN) return fail(ctx, YY_ESTATE, "internal: wall batch overflow");
+      const int q = b.njobs++;
       int nin = 0;
       for (int m = 0; m < ctx->nw[p]; ++m)
         if (ctx->wterm[p][m][f]) {
-          in.p[nin] = ctx->wterm[p][m][f];
-          in.c[nin] = tf_value(ctx->wtf[p][m], t);
+          b.p[q][nin] = ctx->wterm[p][m][f];
+          b.c[q][nin] = tf_value(ctx->wtf[p][m], t);
           ++nin;
         }
-      ProfScope ps(ctx, "walls", 1);
-      launch_lincomb(ctx->wl[L][f] + p * ws, ws, in, nin, ctx->st);
+      b.out[q] = ctx->wl[L][f] + p * ws;
+      b.n[q] = ws;
+      b.nin[q] = nin;
     }
   }
   return YY_OK;
@@ -619,7 +641,10 @@ ResidArgs resid_args(yy_ctx* ctx, int q, int s) {
   r.wn = wf >= 0 ? ctx->wl[1][wf] : nullptr;
   r.ar = ctx->astar[0]; r.at = ctx->astar[1]; r.ap = ctx->astar[2];
   r.rt = ctx->react_t; r.rp = ctx->react_p;
-  if (ctx->imex) r.ar = r.at = r.ap = r.rt = r.rp = ctx->zero;   // split rows without transport terms
+  if (ctx->imex) {   // split rows without transport terms
+    r.ar = r.at = r.ap = r.rt = r.rp = ctx->zero;
+    r.noadv = 1;
+  }
   r.G = ctx->G[f];
   r.R = ctx->R;
   r.Tit = ctx->it[FT]; r.Tn = ctx->n[FT];
@@ -635,7 +660,10 @@ SweepArgs sweep_args(yy_ctx* ctx, int q, int s, int slot) {
   SweepArgs w{};
   w.ar = ctx->astar[0]; w.at = ctx->astar[1]; w.ap = ctx->astar[2];
   w.rt = ctx->react_t; w.rp = ctx->react_p;
-  if (ctx->imex) w.ar = w.at = w.ap = w.rt = w.rp = ctx->zero;
+  if (ctx->imex) {
+    w.ar = w.at = w.ap = w.rt = w.rp = ctx->zero;
+    w.noadv = 1;
+  }
   w.R = ctx->R; w.psi = ctx->it[qfield(q, s)];
   w.part = ctx->part + (long long)slot * 2 * ctx->maxb;
   w.maxb = ctx->maxb;
@@ -718,14 +746,25 @@ yy_status step_begin(yy_ctx* ctx) {
   cudaStream_t st = ctx->st;
   const int NPT = g.npatch;
   // wall data at t_{n-1}, t_n, t_{n+1}
-  for (int L = 0; L < 3; ++L) TRY(eval_walls(ctx, L, t + (L - 1) * tau));
+  {
+    LinBatch b{};
+    for (int L = 0; L < 3; ++L) TRY(eval_walls(ctx, L, t + (L - 1) * tau, b));
+    ProfScope ps(ctx, "walls", 1);
+    launch_lincomb_batch(b, st);
+  }
   // O2: a* = 1.5 u2^n - 0.5 u2^{n-1}
-  for (int c = 0; c < 3; ++c) {
-    LinIn in{};
-    in.p[0] = ctx->n[FUR2 + c]; in.c[0] = 1.5;
-    in.p[1] = ctx->m[FUR2 + c]; in.c[1] = -0.5;
+  {
+    LinBatch b{};
+    for (int c = 0; c < 3; ++c) {
+      b.out[c] = ctx->astar[c];
+      b.p[c][0] = ctx->n[FUR2 + c]; b.c[c][0] = 1.5;
+      b.p[c][1] = ctx->m[FUR2 + c]; b.c[c][1] = -0.5;
+      b.n[c] = NPT * fsize(ctx, FUR2 + c);
+      b.nin[c] = 2;
+    }
+    b.njobs = 3;
     ProfScope ps(ctx, "astar", 1);
-    launch_lincomb(ctx->astar[c], NPT * fsize(ctx, FUR2 + c), in, 2, st);
+    launch_lincomb_batch(b, st);
   }
   if (!ctx->imex) {   // IMEX: the split rows take no transport terms (Geo::adv -> zero)
     ProfScope ps(ctx, "react", 1);
@@ -739,18 +778,34 @@ yy_status step_begin(yy_ctx* ctx) {
     launch_static(g, q, a, st);
   }
   // O4: psi^(0) = psi^n; u_r walls at t_{n+1}
-  for (int f = 0; f < NF; ++f) {
-    ProfScope ps(ctx, "copy_iterate", 0);
-    CK(cudaMemcpyAsync(ctx->it[f], ctx->n[f], NPT * fsize(ctx, f) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  // (two batched copy launches: the iterates, then the wall planes they contain)
+  {
+    LinBatch b{};
+    for (int f = 0; f < NF; ++f) {
+      b.out[b.njobs] = ctx->it[f];
+      b.p[b.njobs][0] = ctx->n[f];
+      b.n[b.njobs] = NPT * fsize(ctx, f);
+      b.nin[b.njobs++] = -1;
+    }
+    ProfScope ps(ctx, "copy_iterate", 1);
+    launch_lincomb_batch(b, st);
   }
-  const long long plane = (long long)g.nt * g.np;
-  for (int f : {FUR1, FUR2})
-    for (int p = 0; p < NPT; ++p)
-      for (int w = 0; w < 2; ++w)
-        if (w ? g.wall_hi : g.wall_lo)     // wall faces ilo_f - 1 (r = R1), ihi_f + 1 (r = R2)
-          CK(cudaMemcpyAsync(ctx->it[f] + p * fsize(ctx, f) + (long long)(w ? g.ihi_f + 1 : g.ilo_f - 1) * plane,
-                             ctx->wl[2][WUR] + (p * 2 + w) * plane, plane * sizeof(double),
-                             cudaMemcpyDeviceToDevice, st));
+  {
+    const long long plane = (long long)g.nt * g.np;
+    LinBatch b{};
+    for (int f : {FUR1, FUR2})
+      for (int p = 0; p < NPT; ++p)
+        for (int w = 0; w < 2; ++w)
+          if (w ? g.wall_hi : g.wall_lo) {   // wall faces ilo_f - 1 (r = R1), ihi_f + 1 (r = R2)
+            b.out[b.njobs] = ctx->it[f] + p * fsize(ctx, f) + (long long)(w ? g.ihi_f + 1 : g.ilo_f - 1) * plane;
+            b.p[b.njobs][0] = ctx->wl[2][WUR] + (p * 2 + w) * plane;
+            b.n[b.njobs] = plane;
+            b.nin[b.njobs++] = -1;
+          }
+    ProfScope ps(ctx, "copy_iterate", 1);
+    launch_lincomb_batch(b, st);
+  }
+  CK(cudaGetLastError());
   return YY_OK;
 }
 
@@ -945,6 +1000,21 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
   if (graph && ctx->use_graph == 2 && cs.size() == 1 && ctx->mode == 0) {
     // the whole loop on the device: a WHILE node whose body is one iteration
     // (O5-O10) followed by k_schwarz_cond; one launch and one host sync per step
+    std::vector<const void*> key;
+    for (int f = 0; f < NF; ++f) { key.push_back(ctx->it[f]); key.push_back(ctx->n[f]); }
+    key.push_back((const void*)(intptr_t)kmax);
+    key.push_back((const void*)(intptr_t)(ctx->fixed_iters > 0));
+    cudaGraphExec_t ge = nullptr;
+    long long per_iter = 0;
+    for (auto& lg : ctx->loop_graphs)
+      if (lg.key == key && lg.tol == tol && lg.rev_in == ctx->rev_next) {
+        ge = lg.exec;
+        per_iter = lg.per_iter;
+        ctx->rev_next = lg.rev_out;
+        break;
+      }
+    if (!ge) {
+    const int rev_in = ctx->rev_next;
     const long long l0 = ctx->launches;
     cudaGraph_t gr = nullptr;
     CK(cudaGraphCreate(&gr, 0));
@@ -973,19 +1043,18 @@ yy_status step_group(std::vector<yy_ctx*>& cs, double tol, int* iters, double* r
     const cudaError_t ec = cudaStreamEndCapture(ctx->st, &body);
     if (sc != YY_OK) { cudaGraphDestroy(gr); return sc; }
     if (ec != cudaSuccess) { cudaGraphDestroy(gr); CK(ec); }
-    const long long per_iter = ctx->launches - l0;   // (incl. k_schwarz_cond)
+    per_iter = ctx->launches - l0;   // (incl. k_schwarz_cond)
     ctx->launches = l0;
-    cudaGraphExec_t ge = nullptr;
     const cudaError_t ei = cudaGraphInstantiate(&ge, gr, 0);
     cudaGraphDestroy(gr);
     CK(ei);
+    if (ctx->loop_graphs.size() >= 16) clear_loop_graphs(ctx);
+    ctx->loop_graphs.push_back({key, tol, rev_in, ctx->rev_next, per_iter, ge});
+    }
     CK(cudaMemsetAsync(ctx->ctl, 0, 3 * sizeof(double), ctx->st));
-    const cudaError_t el = cudaGraphLaunch(ge, ctx->st);
-    if (el != cudaSuccess) { cudaGraphExecDestroy(ge); CK(el); }
+    CK(cudaGraphLaunch(ge, ctx->st));
     CK(cudaMemcpyAsync(ctx->red_host, ctx->ctl, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    const cudaError_t es = cudaStreamSynchronize(ctx->st);
-    cudaGraphExecDestroy(ge);
-    CK(es);
+    CK(cudaStreamSynchronize(ctx->st));
     k = (int)ctx->red_host[0];
     rho = ctx->red_host[1];
     ctx->launches += per_iter * k;
@@ -1528,6 +1597,9 @@ yy_status yy_energy(yy_ctx* ctx, double* out3) {
 
 yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
   if (!ctx) return YY_EINVAL;
+  clear_loop_graphs(ctx);
+  if (ctx->mode == 1)
+    for (yy_ctx* c : ctx->group) if (c && c != ctx) clear_loop_graphs(c);
   switch (key) {
     case YY_CHI:
       if (!(v > 0)) return fail(ctx, YY_EINVAL, "chi must be > 0");
@@ -1609,6 +1681,7 @@ yy_status yy_set_allocator(yy_ctx* ctx, void* (*alloc)(size_t, void*), void (*fr
 
 yy_status yy_set_stream(yy_ctx* ctx, void* stream) {
   if (!ctx) return YY_EINVAL;
+  clear_loop_graphs(ctx);
   ctx->st = static_cast<cudaStream_t>(stream);
   if (ctx->mode == 1)   // a loopback group shares one stream
     for (yy_ctx* c : ctx->group) if (c) c->st = ctx->st;
@@ -1690,6 +1763,7 @@ void yy_destroy(yy_ctx* ctx) {
     if (ctx->alloc_fn) ctx->free_fn(p, ctx->alloc_user);
     else cudaFree(p);
   }
+  for (auto& lg : ctx->loop_graphs) cudaGraphExecDestroy(lg.exec);
   if (ctx->red_host) cudaFreeHost(ctx->red_host);
   for (cudaStream_t a : ctx->aux) if (a) cudaStreamDestroy(a);
   for (cudaEvent_t e : ctx->fork) if (e) cudaEventDestroy(e);

@@ -15,6 +15,18 @@ struct LinIn {               // out = sum_m c[m] * p[m]
   double c[8];
 };
 
+// a batch of small linear combinations in one launch (the wall data of every
+// (time level, field, patch) of a step: 24 launches -> 1)
+constexpr int MAXLIN = 32;
+struct LinBatch {
+  double* out[MAXLIN];
+  long long n[MAXLIN];
+  int nin[MAXLIN];              // terms; -1: a plain copy of p[.][0]
+  const double* p[MAXLIN][4];
+  double c[MAXLIN][4];
+  int njobs;
+};
+
 struct StaticArgs {
   const double* fn[2];       // psi^n   (system 1, 2; T uses [0])
   const double* fm[2];       // psi^{n-1}
@@ -49,6 +61,7 @@ struct ResidArgs {
   const double *p1it, *p1n;
   const double* dp1;         // p1^(k) - p1^n (both patches, fringe incl.) or NULL: from p1it, p1n
   int rev;                   // reverse block order (bidx)
+  int noadv;                 // IMEX: L_split without transport terms (no a* / row-weight reads)
 };
 
 struct SweepArgs {
@@ -67,6 +80,8 @@ struct SweepArgs {
   int vw;                    // write V, W (they depend on the step's matrix only: the first
                              // iteration of a step writes them, later ones reuse them)
   int rev;                   // run the grid's blocks in reverse linear order (bidx)
+  int noadv;                 // IMEX (YY_ADVECTION = 1): rows without transport terms — the
+                             // per-step row weights are not read (16 B per element, 24 final)
 };
 
 // one r-line's slab-coupling solution (yy_slab.cu)
@@ -127,6 +142,7 @@ struct InterpArgs {
 };
 
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);
+void launch_lincomb_batch(const LinBatch& b, cudaStream_t st);
 // per step, after a*: the reaction coefficients rt (TH nodes), rp (PH nodes) of Astar
 void launch_react(const Geo& g, const double* ar, const double* at, double* rt, double* rp, cudaStream_t st);
 // per step, after a*: the transport-velocity row weights Astar::av of the kinds in

@@ -58,6 +58,24 @@ __global__ void k_lincomb(double* __restrict__ out, long long n, int nin, LinIn 
   }
 }
 
+// one job per blockIdx.y, grid-stride in x (same summation order as k_lincomb)
+__global__ void k_lincomb_batch(LinBatch b) {
+  const int jb = blockIdx.y;
+  const long long n = b.n[jb];
+  double* __restrict__ out = b.out[jb];
+  const int nin = b.nin[jb];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    if (nin < 0) {                         // plain copy (bit for bit, signed zeros too)
+      out[idx] = b.p[jb][0][idx];
+      continue;
+    }
+    double v = 0.0;
+    for (int m = 0; m < nin; ++m) v += b.c[jb][m] * b.p[jb][m][idx];
+    out[idx] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // K0: static right-hand side G (O3):  G = tau [L_full psi^* - 1/2 L_split (psi^n - psi^{n-1}) + E_static]
 // grid: x -> k, y -> j, z -> patch * NR + i
@@ -142,7 +160,7 @@ __global__ void __launch_bounds__(128) k_static(Geo g, StaticArgs a) {
 #ifndef YY_RESID_MINB
 #define YY_RESID_MINB 8
 #endif
-template <int Q, int S, int IB>
+template <int Q, int S, int IB, bool NOADV = false>
 __global__ void __launch_bounds__(128, YY_RESID_MINB) k_resid(Geo g, ResidArgs a) {
   const uint3 B = bidx(a.rev);
   // thread = one (j, k) column, IB consecutive r-nodes (setup amortised, r-neighbours
@@ -159,17 +177,25 @@ __global__ void __launch_bounds__(128, YY_RESID_MINB) k_resid(Geo g, ResidArgs a
   // blocks away from the walls (all but the first / last chunk of r-nodes) take
   // no wall-ghost code (a block-uniform branch)
   const bool edge = K != KR && ((g.wall_lo && i0 == g.ilo_c) || (g.wall_hi && i0 + IB - 1 >= g.ihi_c));
-  if (edge) {
+  if constexpr (NOADV) {   // IMEX: split rows without transport terms (separate instantiation)
 #pragma unroll
     for (int u = 0; u < IB; ++u) {
       const int i = i0 + u;
-      if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, true>(g, a, patch, i, j, k);
+      if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, true, true>(g, a, patch, i, j, k);
     }
   } else {
+    if (edge) {
 #pragma unroll
-    for (int u = 0; u < IB; ++u) {
-      const int i = i0 + u;
-      if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, false>(g, a, patch, i, j, k);
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 + u;
+        if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, true>(g, a, patch, i, j, k);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 + u;
+        if (i <= i_hi<K>(g)) R[IX<K>(g, i, j, k)] = resid_at<Q, S, false>(g, a, patch, i, j, k);
+      }
     }
   }
 }
@@ -653,6 +679,15 @@ static inline dim3 pgrid(const Geo& g, int K, int npatch) {
   return dim3((NPk(g, K) + 127) / 128, NTk(g, K), NRk(g, K) * npatch);
 }
 
+void launch_lincomb_batch(const LinBatch& b, cudaStream_t st) {
+  if (b.njobs <= 0) return;
+  long long mx = 0;
+  for (int q = 0; q < b.njobs; ++q) mx = b.n[q] > mx ? b.n[q] : mx;
+  const long long nb = (mx + 255) / 256;
+  const int bx = (int)(nb < 148 ? nb : 148);
+  k_lincomb_batch<<<dim3(bx > 0 ? bx : 1, b.njobs), 256, 0, st>>>(b);
+}
+
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
@@ -675,7 +710,8 @@ void resid_qb(const Geo& g, const ResidArgs& a, cudaStream_t st) {
   const int nch = (i_hi<K>(g) - i_lo<K>(g) + IB) / IB;
   constexpr int BK = YY_RESID_BK, BJ = 128 / BK;
   const dim3 grid((NPk(g, K) - 2 + BK - 1) / BK, (NTk(g, K) - 2 + BJ - 1) / BJ, g.npatch * nch);
-  k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
+  if (a.noadv) k_resid<Q, S, IB, true><<<grid, 128, 0, st>>>(g, a);
+  else k_resid<Q, S, IB><<<grid, 128, 0, st>>>(g, a);
 }
 // r-nodes per thread of the residual per (quantity, system), measured on B200
 // (C3): T 2, u_r 2 / 1, u_th 2 / 2, u_ph 4 / 4.  YY_RESID_IB=<T>,<ur1>,<ur2>,<ut1>,

@@ -35,12 +35,17 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "yy_dev.cuh"
 #include "yy_internal.h"
 #include "yy_stencil.cuh"
 
 #ifndef YY_LINE_MINB
 #define YY_LINE_MINB 0   // >0: force this __launch_bounds__ min blocks per SM (tuning)
+#endif
+#ifndef YY_IMEX_FAST
+#define YY_IMEX_FAST 1   // IMEX rows without the per-step weight reads (0: IMEX reads the zero arrays)
 #endif
 #ifndef YY_RT_MENU
 #define YY_RT_MENU 0     // r / theta chunkings for n <= 128: 0 (16,6)/(16,8); 1 (8,12)/(8,16); 2 (32,3)/(32,4)
@@ -324,12 +329,16 @@ enum { MODE_PLAIN = 0, MODE_FIRST = 1, MODE_FINAL = 2, MODE_SLAB = 3 };
 #ifndef YY_MINB_16
 #define YY_MINB_16 5        // r/theta (16, 6) / (16, 8) tiles
 #endif
+#ifndef YY_MINB_M16
+#define YY_MINB_M16 3       // chunks of 13-16 rows (C5 theta (16,16)): 168 registers, no spill (measured
+                            // faster than 4 blocks at 128 registers with a 76 B spill: C5 100 -> 96 ms/step)
+#endif
 constexpr int line_minb(int P, int M) {
   return YY_LINE_MINB > 0 ? YY_LINE_MINB
          : P > 32 ? (M <= 6 ? YY_MINB_MW : 4)   // multi-warp phi lines (part_solve3: 3 live arrays)
          : (P == 32 && M == 12) ? YY_MINB_3212
          : (P == 16 && M <= 8) ? YY_MINB_16
-                  : (M <= 12 ? 5 : M <= 16 ? 4 : M <= 24 ? 2 : 1);
+                  : (M <= 12 ? 5 : M <= 16 ? YY_MINB_M16 : M <= 24 ? 2 : 1);
 }
 
 template <int Q, int AX, int MODE, int S, int P, int M>
@@ -438,7 +447,11 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       elem(u, l, e);
       const int s = slot(l, e);
       if (AX == 2 && AVG) {
-        if (e < n) {
+        if (e < n && a.noadv) {           // IMEX: no transport terms in the rows
+          cp_async8(RH + s, Rb + e);
+          LO[s] = 0.0;
+          UP[s] = 0.0;
+        } else if (e < n) {
           cp_async8(RH + s, Rb + e);
           cp_async8(LO + s, Vb + e);
           if (RXR) cp_async8(UP + s, Xb + e);
@@ -475,12 +488,14 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     // the transport-velocity rows coef<> reads for these elements go to L1 first
     // (no registers held), so make_row below finds them there instead of paying a
     // DRAM round trip per element
+    if (!a.noadv) {
 #pragma unroll
-    for (int u = 0; u < M; ++u) {
-      int l, e, i, j, k;
-      elem(u, l, e);
-      node(l, min(e, n - 1), i, j, k);
-      prefetch_rows<Q, AX>(g, A, i, j, k);
+      for (int u = 0; u < M; ++u) {
+        int l, e, i, j, k;
+        elem(u, l, e);
+        node(l, min(e, n - 1), i, j, k);
+        prefetch_rows<Q, AX>(g, A, i, j, k);
+      }
     }
     double rv[M];
 #pragma unroll
@@ -489,25 +504,39 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       elem(u, l, e);
       rv[u] = R[node(l, min(e, n - 1), i, j, k)];
     }
+    // (the IMEX branch is taken once per block, outside the unrolled rows, so the
+    // default path keeps its load batching)
+    auto build = [&](auto noadv) {
 #pragma unroll
-    for (int u = 0; u < M; ++u) {
-      int l, e, i, j, k;
-      elem(u, l, e);
-      const int ec = min(e, n - 1);
-      node(l, ec, i, j, k);
-      double lo, up, rh;
-      make_row<Q, AX>(g, A, i, j, k, ec, n, rv[u], lo, up, rh, MODE == MODE_SLAB);
-      const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
-      const int s = slot(l, e);
-      LO[s] = lo * mk;
-      UP[s] = up * mk;
-      RH[s] = rh * mk;
-    }
+      for (int u = 0; u < M; ++u) {
+        int l, e, i, j, k;
+        elem(u, l, e);
+        const int ec = min(e, n - 1);
+        node(l, ec, i, j, k);
+        double lo, up, rh;
+        if constexpr (decltype(noadv)::value)   // IMEX: the a* = 0 rows, no per-step weight read
+          make_row<Q, AX, RX_GIVEN>(g, A, i, j, k, ec, n, rv[u], lo, up, rh, MODE == MODE_SLAB, 0.0, 0.0);
+        else
+          make_row<Q, AX>(g, A, i, j, k, ec, n, rv[u], lo, up, rh, MODE == MODE_SLAB);
+        const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
+        const int s = slot(l, e);
+        LO[s] = lo * mk;
+        UP[s] = up * mk;
+        RH[s] = rh * mk;
+      }
+    };
+#if YY_IMEX_FAST
+    if (a.noadv) build(std::true_type{});
+    else
+#endif
+      build(std::false_type{});
   }
   // r/theta final sweeps (YY_PSI_EARLY): psi of the tile is loaded into registers
   // before the solve, so its DRAM latency overlaps the solve
   double pv[M];
-  constexpr bool PSE = FINAL && AX != 2 && YY_PSI_EARLY;
+  // (chunks of more than 8 rows keep psi out of the solve's registers: the
+  // u_theta (16,16) final sweep of C5 spilled 144 B with it)
+  constexpr bool PSE = FINAL && AX != 2 && YY_PSI_EARLY && M <= 8;
   if (PSE) {
 #pragma unroll
     for (int u = 0; u < M; ++u) {

@@ -93,7 +93,7 @@ __device__ __forceinline__ double div3(const Geo& g, const double* up, int i, in
 //   R = G + tau E_dyn - (I - tau/2 L_split)(psi~ - psi^n)
 // with the Gauss-Seidel dynamic terms E_dyn of SURVEY §8(c) O7/O9 (RD20, RD21,
 // RD18, RD-E1).
-template <int Q, int S, bool WALL = true>
+template <int Q, int S, bool WALL = true, bool NOADV = false>
 __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int patch, int i, int j, int k) {
   constexpr int K = kind_of(Q);
   const long long po = patch * psize(g, K);
@@ -172,7 +172,8 @@ __device__ __forceinline__ double resid_at(const Geo& g, const ResidArgs& a, int
     if (Q == QUT) E -= 0.5 * (dp(i, j, k) - dp(i, j - 1, k)) * (__ldg(g.ir_c + i) * g.idth);
     if (Q == QUP) E -= 0.5 * (dp(i, j, k) - dp(i, j, k - 1)) * (__ldg(g.ir_c + i) * __ldg(g.is_c + j) * g.idph);
   }
-  const double LX = applyL<Q, true, RX_RESID>(g, A, i, j, k, X);
+  // IMEX (NOADV): the split rows without transport terms, no per-step weight read
+  const double LX = NOADV ? applyL<Q, true, RX_GIVEN>(g, A, i, j, k, X) : applyL<Q, true, RX_RESID>(g, A, i, j, k, X);
   return __ldg(a.G + po + node) + g.tau * E - (X.c - 0.5 * g.tau * LX);
 }
 

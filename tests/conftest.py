@@ -31,18 +31,20 @@ def pytest_collection_modifyitems(config, items):
 
 
 def pytest_sessionfinish(session, exitstatus):
-    """Write the per-field parity metric of every GPU parity test (BASELINE.md
-    §2) next to the run's other GPU evidence when gpurun_out/ exists."""
-    try:
-        import json
-        from tests import test_gpu_parity as tp   # noqa: F401
-    except Exception:
-        try:
-            import json
-            import test_gpu_parity as tp          # noqa: F401
-        except Exception:
-            return
+    """Write the parity numbers of the GPU tests (per-field metric of every parity
+    test; K and worst sampled error of every full-size golden case)
+    next to the run's other GPU evidence when gpurun_out/ exists."""
+    import importlib
+    import json
     out = os.path.join(ROOT, "gpurun_out")
-    if tp.PER_FIELD and os.path.isdir(out):
-        with open(os.path.join(out, "parity_per_field.json"), "w") as fh:
-            json.dump(tp.PER_FIELD, fh, indent=1)
+    if not os.path.isdir(out):
+        return
+    for mod, attr, fname in (("test_gpu_parity", "PER_FIELD", "parity_per_field.json"),
+                             ("test_gpu_fullsize", "RESULTS", "fullsize_parity.json")):
+        m = sys.modules.get(mod) or sys.modules.get("tests." + mod)
+        if m is None:
+            continue
+        data = getattr(m, attr, None)
+        if data:
+            with open(os.path.join(out, fname), "w") as fh:
+                json.dump(data, fh, indent=1)

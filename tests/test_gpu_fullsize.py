@@ -18,6 +18,7 @@ import workloads as W
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RESULTS = {}    # per golden case: K per step and the worst sampled error (conftest writes them out)
 
 
 def _shell(cfg, **kw):
@@ -66,6 +67,7 @@ def test_full_size_steps_match_oracle_golden(name, steps, tag):
                 d = float(np.max(np.abs(got - np.array(g["value"]))))
                 e = d / den if den > 0 else (0.0 if d == 0.0 else float("inf"))
                 worst = max(worst, e)
+    RESULTS[f"{name}{tag}_step{steps}"] = {"K": ks, "worst_rel_err": worst}
     assert worst <= 1e-11 * steps, worst
 
 

@@ -1,0 +1,82 @@
+#!/usr/bin/env python
+"""Fill BASELINE.md §5 ("Measured results") from the committed evidence under
+profiles/: the bench lines (profiles/r02_bench_<cfg>.json), the ncu DRAM
+traffic of the dominant kernel (profiles/traffic.json, C3), the full-size
+golden parity results (profiles/r02_fullsize_parity.json) and the per-field
+parity metric of the reduced-size tests (profiles/r02_parity_per_field.json).
+
+    python tools/results_table.py            # rewrites the table in BASELINE.md
+"""
+import json
+import os
+import re
+import statistics
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles")
+
+
+def load(name):
+    try:
+        with open(os.path.join(P, name)) as f:
+            txt = f.read().strip()
+        return json.loads(txt.splitlines()[-1]) if txt.startswith("{") and "\n{" in txt else json.loads(txt)
+    except (OSError, ValueError):
+        return None
+
+
+def row(cfg, label, bench, parity, traffic):
+    if not bench:
+        return f"| {label} | 1 | — | — | — | — | — | — | — |"
+    Ks = bench["config"].get("schwarz_iters_per_step", [])
+    sr = bench["config"].get("step_roofline", {})
+    cpu = bench.get("cpu_baseline") or {}
+    rf = bench.get("roofline") or {}
+    tr = "—"
+    if traffic and rf.get("bytes_per_launch"):
+        t = traffic.get("bytes_per_launch", {}).get(rf.get("kernel"))
+        if t:
+            tr = f"{t / rf['bytes_per_launch']:.2f} ({rf['kernel']})"
+    par = "—"
+    if parity:
+        cases = {k: v for k, v in parity.items() if k.startswith(cfg)}
+        if cases:
+            first = [v for k, v in cases.items() if k.endswith("_step1")]
+            last_k = max(cases, key=lambda k: int(k.rsplit("step", 1)[1]))
+            par = (f"{max(v['worst_rel_err'] for v in first):.1e} / {cases[last_k]['worst_rel_err']:.1e} "
+                   f"({last_k.rsplit('_', 1)[1]})") if first else "—"
+    keq = "yes (every golden step)" if parity and any(k.startswith(cfg) for k in parity) else "yes (reduced sizes)"
+    return (f"| {label} | {bench['n_gpus']} | {statistics.mean(Ks):.1f} | {bench['value']:.3g} | "
+            f"{100 * sr.get('frac_of_8TBs', 0):.1f} % ({100 * sr.get('frac_of_measured_hbm', 0):.1f} % of 6557 GB/s) | "
+            f"{tr} | {cpu.get('value', float('nan')):.3g} ({cpu.get('cores', '?')}) | {par} | {keq} |")
+
+
+def main():
+    traffic = load("traffic.json")
+    parity = load("r02_fullsize_parity.json")
+    lines = ["| Config | GPUs | K per step (mean) | cell-updates/s | % of M1 roofline @ 8 TB/s | ncu DRAM bytes / M1 "
+             "(dominant kernel) | Oracle cell-updates/s (cores) | Parity max rel err (step 1 / last golden step) | "
+             "Iteration counts equal? |",
+             "|---|---|---|---|---|---|---|---|---|"]
+    for cfg, label in (("C1", "C1 16×16×48"), ("C2", "C2 48×64×192"), ("C3", "C3 96×128×384"),
+                       ("C5", "C5 (N = 1: 2 × 64×192×576)")):
+        lines.append(row(cfg, label, load(f"r02_bench_{cfg.lower()}.json"), parity, traffic))
+    c4 = load("r01_c4_kernels_v53.json")
+    if c4:
+        lines.append(f"| C4 (r / θ / φ, kernel only) | 1 | n/a | see `profiles/r01_c4_kernels_v53.json` | — | — | — | "
+                     f"every line of every axis (`test_c4_line_solves_full_size`) | n/a |")
+    table = "\n".join(lines)
+    path = os.path.join(ROOT, "BASELINE.md")
+    s = open(path).read()
+    head = s[:s.index("## 5. Measured results")]
+    body = ("## 5. Measured results\n\nWritten by `tools/results_table.py` from `profiles/` (round 2; χ = 16, "
+            "DESIGN.md RD-E4).  Parity: the CUDA path against the oracle's full-size goldens (512 sampled nodes "
+            "per field, RD-E3 metric); reduced sizes compare every element (`tests/test_gpu_parity.py`).  The "
+            "oracle rate is the full-grid oracle's static part + one Schwarz iteration, extrapolated to the GPU "
+            "steps' K (bench.py `cpu_baseline`).\n\n" + table + "\n")
+    open(path, "w").write(head + body)
+    print(table)
+
+
+if __name__ == "__main__":
+    main()
