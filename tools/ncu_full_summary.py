@@ -52,6 +52,25 @@ def main(path):
         gbs = f"{mb * 1e6 / (t_us * 1e-6) / 1e9:.0f}" if (t_us and mb) else "-"
         name = r[h.index("Kernel Name")].replace("void ", "").split("(")[0]
         print(f"| `{name}` | {r[h.index('Grid Size')]} | " + " | ".join(vals) + f" | {gbs} |")
+    # warp-state breakdown: cycles a warp spends per issued instruction, by reason
+    st = [i for i, x in enumerate(h) if x.startswith("smsp__average_warps_issue_stalled_")
+          and x.endswith("_per_issue_active.ratio")]
+    if st:
+        print()
+        print("Warp stall reasons (cycles per issued instruction, top 5 per launch):")
+        print()
+        print("| kernel | top stall reasons |")
+        print("|---|---|")
+        for r in rows[2:]:
+            vals = []
+            for i in st:
+                try:
+                    vals.append((float(r[i].replace(",", "")), h[i][34:-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+            vals.sort(reverse=True)
+            name = r[h.index("Kernel Name")].replace("void ", "").split("(")[0]
+            print(f"| `{name}` | " + ", ".join(f"{b} {a:.2f}" for a, b in vals[:5]) + " |")
 
 
 if __name__ == "__main__":
