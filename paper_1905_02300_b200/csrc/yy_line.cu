@@ -31,6 +31,8 @@
 // weights and reaction values staged in shared memory with cp.async; lines
 // longer than 384 rows take four warps (segments with symbolic couplings, then
 // the line's 8-unknown boundary system, as for radial slabs).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -713,10 +715,251 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
 }
 
 // ---------------------------------------------------------------------------------
+// theta sweeps with TMA-staged tiles (plain and final factors).
+// The same tile (NL = 128/P consecutive k-lines of one (j | i, patch)) and the same
+// chunk algebra as k_line, but the tile's inputs (right-hand side, row weight
+// Astar::av, the u_theta reaction, FINAL psi) arrive by cp.async.bulk.tensor
+// (one elected thread, one mbarrier) as [row][line] boxes in shared memory, and
+// the result leaves by a bulk tensor store: the global traffic bypasses the LSU /
+// L1 data pipe, which ncu shows at ~73 % of its wavefront peak in k_line
+// (profiles/r02_ncu.md).  The build reads four consecutive rows of eight lines per
+// warp instruction (256 contiguous bytes: conflict-free), so its 1-D table reads
+// are one wavefront.  Eligible kinds: row pitch a multiple of 16 B (nphi even;
+// the u_phi kind's nphi + 1 is not — it keeps k_line).
+// ---------------------------------------------------------------------------------
+struct TmaMaps {
+  CUtensorMap m[4];          // rhs (R), Astar::av, reaction rt (u_theta theta), psi (FINAL)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];"
+               ::"l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+template <int Q, int AX, bool FINAL>
+__host__ __device__ constexpr int tma_narr() { return 2 + ((Q == QUT && AX == 1) ? 1 : 0) + (FINAL ? 1 : 0); }
+
+template <int Q, int AX, int MODE, int P, int M>
+__global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepArgs a, const __grid_constant__ TmaMaps maps) {
+  static_assert(AX != 2 && (MODE == MODE_PLAIN || MODE == MODE_FINAL), "r / theta plain or final sweeps");
+  static_assert(use_av(Q, AX, RX_SWEEP), "the staged rows take the per-step weights Astar::av");
+  const uint3 B = bidx(a.rev);
+  constexpr bool FINAL = (MODE == MODE_FINAL);
+  constexpr bool RXR = (Q == QUT && AX == 1);
+  constexpr int K = kind_of(Q);
+  constexpr int NL = 128 / P;
+  constexpr int MP = M | 1;
+  constexpr int LP = line_pitch<P, MP>();
+  constexpr int NPAD = P * M;
+  constexpr int SA = (NPAD * NL + 15) / 16 * 16;      // one staged array (128-B multiple)
+  constexpr int NA = tma_narr<Q, AX, FINAL>();
+  // the staged inputs (FINAL: rhs; av; reaction) and the chunk-major solve tile
+  // share the front of shared memory (the inputs are read into registers first);
+  // the box that is written back follows — FINAL psi, PLAIN the rhs itself — so
+  // that the phi-fringe columns of the tile (k = 0, nphi - 1) go back unchanged
+  constexpr int NIN = NA - 1;
+  constexpr int FRONT = NIN * SA > 3 * NL * LP ? NIN * SA : 3 * NL * LP;
+  extern __shared__ __align__(128) double sm[];
+  double* Sps = sm + (FRONT + 15) / 16 * 16;          // [row][line] boxes: psi (FINAL) / rhs (PLAIN)
+  double* Srh = FINAL ? sm : Sps;
+  double* Sav = sm + (FINAL ? SA : 0);
+  double* Srx = Sav + SA;
+  double* LO = sm;                                    // chunk-major solve tile (as k_line)
+  double* UP = LO + NL * LP;
+  double* RH = UP + NL * LP;
+  __shared__ __align__(8) uint64_t bar;
+  const int patch = B.z;
+  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
+  // tiles start at k = 0 (the phi-fringe column, an identity line): a bulk tensor
+  // box must start on a 16-B boundary, i.e. at an even k for fp64 (measured: an odd
+  // start is an illegal instruction, tools/tma_align_probe.cu)
+  const int k0 = B.x * NL;
+  auto lvalid = [&](int l) { return k0 + l >= 1 && k0 + l <= NPk(g, K) - 2; };
+  int i0, j0;
+  if (AX == 0) { i0 = i_lo<K>(g); j0 = B.y + 1; }
+  else { i0 = B.y + i_lo<K>(g); j0 = 1; }
+  // box origin (k, j, patch-folded r row)
+  const int c0 = k0, c1 = j0, c2 = patch * NRk(g, K) + i0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)(NA * n * NL * sizeof(double));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes) : "memory");
+    tma_load_3d(Srh, &maps.m[0], &bar, c0, c1, c2);
+    tma_load_3d(Sav, &maps.m[1], &bar, c0, c1, c2);
+    if (RXR) tma_load_3d(Srx, &maps.m[2], &bar, c0, c1, c2);
+    if (FINAL) tma_load_3d(Sps, &maps.m[3], &bar, c0, c1, c2);
+  }
+  (void)NIN;
+  __syncthreads();                                    // the barrier is initialised
+  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
+          a.rt + patch * psize(g, KT), a.rp + patch * psize(g, KP)};
+  bind_adv<K>(g, A, patch);
+  const int lt = threadIdx.x % NL, rg = threadIdx.x / NL;   // build / write-back: line, row group
+  const int kk = min(max(k0 + lt, 1), NPk(g, K) - 2);
+  auto slot = [&](int l, int e) { return l * LP + (e / M) * MP + (e % M); };
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n"
+      ::"r"(smem_u32(&bar)) : "memory");
+  // 1. build: element u of this thread is row e = u P + rg of line lt; the staged
+  //    values go to registers first (their space is the solve tile's)
+  double vr[M], va[M], vx[M];
+#pragma unroll
+  for (int u = 0; u < M; ++u) {
+    const int q = min(u * P + rg, n - 1) * NL + lt;
+    vr[u] = Srh[q];
+    va[u] = a.noadv ? 0.0 : Sav[q];
+    vx[u] = (RXR && !a.noadv) ? Srx[q] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < M; ++u) {
+    const int e = u * P + rg;
+    const int ec = min(e, n - 1);
+    const int i = (AX == 0) ? i0 + ec : i0, j = (AX == 0) ? j0 : j0 + ec;
+    double lo, up, rh;
+    make_row<Q, AX, RX_GIVEN>(g, A, i, j, kk, ec, n, vr[u], lo, up, rh, false, va[u], vx[u]);
+    const double mk = (e < n && lvalid(lt)) ? 1.0 : 0.0;
+    const int s = slot(lt, e);
+    LO[s] = lo * mk;
+    UP[s] = up * mk;
+    RH[s] = rh * mk;
+  }
+  __syncthreads();
+  // 2.-3. solve chunk c of line l (as k_line)
+  {
+    const int l = threadIdx.x / P, c = threadIdx.x % P;
+    const int o = l * LP + c * MP;
+    double lo[M], up[M], rh[M];
+#pragma unroll
+    for (int u = 0; u < M; ++u) {
+      lo[u] = LO[o + u];
+      up[u] = UP[o + u];
+      rh[u] = RH[o + u];
+    }
+    part_solve<P, M>(lo, up, rh, c);
+#pragma unroll
+    for (int u = 0; u < M; ++u) RH[o + u] = rh[u];
+  }
+  __syncthreads();
+  // 4. the result into the [row][line] box (FINAL: psi + x and the norm), then one
+  //    bulk tensor store (rows past n lie outside the box; the fringe columns
+  //    k = 0, nphi - 1 carry x = 0, i.e. they write back their own values)
+  double wsum = 0.0;
+  double* out = Sps;
+#pragma unroll
+  for (int u = 0; u < M; ++u) {
+    const int e = u * P + rg;
+    if (e < n && lvalid(lt)) {
+      const int q = e * NL + lt;
+      const double x = RH[slot(lt, e)];
+      if (FINAL) {
+        out[q] = Sps[q] + x;
+        const int i = (AX == 0) ? i0 + e : i0, j = (AX == 0) ? j0 : j0 + e;
+        const double r = rnode<K>(g, i), sn = snode<K>(g, j);
+        wsum += r * r * sn * x * x;
+      } else {
+        out[q] = x;
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(FINAL ? &maps.m[3] : &maps.m[0], out, c0, c1, c2);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  if (FINAL) {
+    wsum *= g.dr * g.dth * g.dph;
+    __shared__ double sh[4];
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_down_sync(FULL, wsum, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      a.part[(long long)patch * a.maxb + B.y * gridDim.x + B.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// host: a 3-D tensor map over every patch of one kind-K array (dims phi, theta,
+// patch-folded r), box = one tile (NL lines x n rows along AX)
+inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, int K, int npatch, int AX, int NL,
+                            int n) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)NPk(g, K), (cuuint64_t)NTk(g, K), (cuuint64_t)NRk(g, K) * npatch};
+  const cuuint64_t strides[2] = {(cuuint64_t)NPk(g, K) * 8, (cuuint64_t)NTk(g, K) * NPk(g, K) * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)NL, (cuuint32_t)(AX == 1 ? n : 1), (cuuint32_t)(AX == 0 ? n : 1)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// env YY_TMA (default 1): theta plain and final sweeps of the TMA-eligible kinds on k_line_tma
+inline bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("YY_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int Q, int AX, int MODE, int P, int M>
+int launch_tma(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  constexpr int NL = 128 / P;
+  constexpr bool FINAL = (MODE == MODE_FINAL);
+  constexpr int SA = (P * M * NL + 15) / 16 * 16;
+  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
+  if ((NPk(g, K) % 2) || n > 256) return -1;          // row pitch a multiple of 16 B; box rows <= 256
+  TmaMaps maps{};
+  const long long off = 0;
+  bool ok = encode_tile_map(&maps.m[0], a.R + off, g, K, npatch, AX, NL, n) &&
+            encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, NL, n);
+  if (ok && Q == QUT && AX == 1) ok = encode_tile_map(&maps.m[2], a.rt, g, K, npatch, AX, NL, n);
+  if (ok && FINAL) ok = encode_tile_map(&maps.m[3], a.psi, g, K, npatch, AX, NL, n);
+  if (!ok) return -1;
+  constexpr int NIN = tma_narr<Q, AX, FINAL>() - 1;
+  constexpr int TILE = 3 * NL * line_pitch<P, (M | 1)>();
+  constexpr int FRONT = (NIN * SA > TILE ? NIN * SA : TILE + 15) / 16 * 16;
+  const size_t smem = ((size_t)FRONT + SA) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_line_tma<Q, AX, MODE, P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const dim3 grid((NPk(g, K) - 1 + NL - 1) / NL, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
+  k_line_tma<Q, AX, MODE, P, M><<<grid, 128, smem, st>>>(g, a, maps);
+  return (int)(grid.x * grid.y);
+}
+
+// ---------------------------------------------------------------------------------
 // launch: pick (P, M) with P*M >= n
 // ---------------------------------------------------------------------------------
 template <int Q, int AX, int MODE, int S, int P, int M>
 int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch, cudaStream_t st) {
+  // theta sweeps only: measured on B200 (C3) the theta classes gain 3-9 %, the r
+  // sweeps lose up to 12 % (their box rows lie 393 KB apart)
+  if constexpr (AX == 1 && (MODE == MODE_PLAIN || MODE == MODE_FINAL) && P <= 32 && M <= 8) {
+    if (use_tma()) {
+      const int nb = launch_tma<Q, AX, MODE, P, M>(g, a, npatch, st);
+      if (nb >= 0) return nb;
+    }
+  }
   constexpr int K = kind_of(Q);
   constexpr int NL = 128 / P;
   // a slab line continued by the slab above must fill its chunks exactly (part_solve3)

@@ -33,22 +33,23 @@ def row(cfg, label, bench, parity, traffic):
     cpu = bench.get("cpu_baseline") or {}
     rf = bench.get("roofline") or {}
     tr = "—"
-    if traffic and rf.get("bytes_per_launch"):
+    if traffic and rf.get("bytes_per_launch") and cfg == "C3":     # the ncu capture is of C3
         t = traffic.get("bytes_per_launch", {}).get(rf.get("kernel"))
         if t:
             tr = f"{t / rf['bytes_per_launch']:.2f} ({rf['kernel']})"
     par = "—"
     if parity:
-        cases = {k: v for k, v in parity.items() if k.startswith(cfg)}
+        cases = {k: v for k, v in parity.items() if k.startswith(cfg + "_chi16")}
         if cases:
             first = [v for k, v in cases.items() if k.endswith("_step1")]
             last_k = max(cases, key=lambda k: int(k.rsplit("step", 1)[1]))
             par = (f"{max(v['worst_rel_err'] for v in first):.1e} / {cases[last_k]['worst_rel_err']:.1e} "
                    f"({last_k.rsplit('_', 1)[1]})") if first else "—"
-    keq = "yes (every golden step)" if parity and any(k.startswith(cfg) for k in parity) else "yes (reduced sizes)"
+    keq = ("yes (every golden step)" if parity and any(k.startswith(cfg + "_chi16") for k in parity)
+           else "yes (reduced sizes)")
     return (f"| {label} | {bench['n_gpus']} | {statistics.mean(Ks):.1f} | {bench['value']:.3g} | "
             f"{100 * sr.get('frac_of_8TBs', 0):.1f} % ({100 * sr.get('frac_of_measured_hbm', 0):.1f} % of 6557 GB/s) | "
-            f"{tr} | {cpu.get('value', float('nan')):.3g} ({cpu.get('cores', '?')}) | {par} | {keq} |")
+            f"{tr} | {('%.3g (%s)' % (cpu['value'], cpu['cores'])) if cpu else '—'} | {par} | {keq} |")
 
 
 def main():
