@@ -18,14 +18,19 @@ def main(path, idx, elems=None):
     ie, isrc = h.index("Instructions Executed"), h.index("Source")
     hist = {}
     for r in rows[2:]:
+        if len(r) <= max(ie, isrc):
+            continue
         src = r[isrc].split()
         if not src:
             continue
         op = src[1] if src[0].startswith("@") else src[0]
         op = op.split(".")[0]
+        if not (r[ie] or "0").isdigit():     # a repeated header (several source sections)
+            continue
         hist[op] = hist.get(op, 0) + int(r[ie] or 0)
     tot = sum(hist.values())
-    print(f"`{name.split('(')[0]}`: {tot:.3g} warp instructions" +
+    name = name.replace("(int)", "").replace("void ", "").split("(")[0]
+    print(f"`{name}`: {tot:.3g} warp instructions" +
           (f", {32 * tot / elems:.1f} thread instructions per element" if elems else ""))
     print()
     print("| opcode | warp inst | share |" + (" per element |" if elems else ""))
