@@ -25,8 +25,8 @@ def main(path, idx, elems=None):
             continue
         op = src[1] if src[0].startswith("@") else src[0]
         op = op.split(".")[0]
-        if not (r[ie] or "0").isdigit():     # a repeated header (several source sections)
-            continue
+        if not (r[ie] or "0").isdigit():     # a second source section repeats the SASS: stop
+            break
         hist[op] = hist.get(op, 0) + int(r[ie] or 0)
     tot = sum(hist.values())
     name = name.replace("(int)", "").replace("void ", "").split("(")[0]
