@@ -411,7 +411,27 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     i = li; j = lj; k = 1 + e;
     return lnd + e;
   };
-  auto slot = [&](int l, int e) { return l * LP + (e / M) * MP + (e % M); };
+  // chunk-major slot of row e of line l.  r/theta elements come from elem(), so
+  // e = c1 M + u and the slot is lt LP + c1 MP + u: one base per thread, the row
+  // an immediate (no division by M per element)
+  const int sbase = lt * LP + c1 * MP;
+  auto slot = [&](int l, int e) {
+    if constexpr (AX != 2) return sbase + (e - c1 * M);
+    else return l * LP + (e / M) * MP + (e % M);
+  };
+  // the same for element u of elem(): phi rows e = lane + P u, so e / M and e % M
+  // follow from lane / M, lane % M (once) and the compile-time (P u) / M, (P u) % M
+  const int lane_ = (AX == 2) ? (int)(threadIdx.x % P) : 0;
+  const int q0 = lane_ / M, r0 = lane_ % M, lb = (AX == 2) ? (int)(threadIdx.x / P) * LP : 0;
+  auto slot_u = [&](int u) {
+    if constexpr (AX != 2) {
+      return sbase + u;
+    } else {
+      int r = r0 + (P * u) % M, q = q0 + (P * u) / M;
+      if (r >= M) { r -= M; ++q; }
+      return lb + q * MP + r;
+    }
+  };
   // 1. build
   if (MODE == MODE_FIRST) {
     // fused eq:er residual: one element at a time (its stencil loads are many and
@@ -426,7 +446,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       double lo, up, rh;
       make_row<Q, AX>(g, A, i, j, k, ec, n, rv, lo, up, rh);
       const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
-      const int s = slot(l, e);
+      const int s = slot_u(u);
       LO[s] = lo * mk;
       UP[s] = up * mk;
       RH[s] = rh * mk;
@@ -447,7 +467,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     for (int u = 0; u < M; ++u) {
       int l, e, i, j, k;
       elem(u, l, e);
-      const int s = slot(l, e);
+      const int s = slot_u(u);
       if (AX == 2 && AVG) {
         if (e < n && a.noadv) {           // IMEX: no transport terms in the rows
           cp_async8(RH + s, Rb + e);
@@ -477,7 +497,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       elem(u, l, e);
       const int ec = min(e, n - 1);
       node(l, ec, i, j, k);
-      const int s = slot(l, e);
+      const int s = slot_u(u);
       double lo, up, rh;
       make_row<Q, AX, AVG ? RX_GIVEN : RX_SWEEP>(g, A, i, j, k, ec, n, RH[s], lo, up, rh, MODE == MODE_SLAB,
                                                  AVG ? LO[s] : 0.0, (AVG && RXR) ? UP[s] : 0.0);
@@ -521,7 +541,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
         else
           make_row<Q, AX>(g, A, i, j, k, ec, n, rv[u], lo, up, rh, MODE == MODE_SLAB);
         const double mk = exists(l, e) ? 1.0 : 0.0;     // identity row outside the tile
-        const int s = slot(l, e);
+        const int s = slot_u(u);
         LO[s] = lo * mk;
         UP[s] = up * mk;
         RH[s] = rh * mk;
@@ -655,7 +675,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
       int l, e;
       elem(u, l, e);
       if (lv && e < n) {
-        const double x = RH[slot(l, e)];
+        const double x = RH[slot_u(u)];
         if (FINAL) {
           Pw[e] = pv[u] + x;
           wsum += rs * x * x;
@@ -679,7 +699,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
     elem(u, l, e);
     if (exists(l, e)) {
       const int nd = node(l, e, i, j, k);
-      const double x = RH[slot(l, e)];
+      const double x = RH[slot_u(u)];
       if (FINAL) {
         a.psi[po + nd] = pv[u] + x;
         const double r = rnode<K>(g, i), s = snode<K>(g, j);
@@ -689,7 +709,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line(Geo g, SweepArgs 
         double* f = (e == 0 || e == n - 1)    // this slab's boundary rows of the line
                         ? a.IF + 6LL * ((j - 1) * (NPk(g, K) - 2) + (k - 1)) + (e == 0 ? 0 : 3) : nullptr;
         if (a.vw) {                           // (per step: the line's responses to its couplings)
-          const double xl = LO[slot(l, e)], xh = UP[slot(l, e)];
+          const double xl = LO[slot_u(u)], xh = UP[slot_u(u)];
           a.V[po + nd] = xl;
           a.W[po + nd] = xh;
           if (f) { f[1] = xl; f[2] = xh; }

@@ -318,3 +318,38 @@ def test_loopback_group_graph_is_bitwise_the_stream_path(nslab):
     for a, b in zip(fa, fb):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_c5_layouts_match_oracle_full_r(G):
+    """The C5 weak-scaling layouts of G GPUs (BASELINE configs[4], SURVEY §8(e):
+    patch Nr = 64 G, Yin on ranks 0..G/2-1 and Yang on the others, G/2 radial
+    slabs of 128 rows per patch; G = 2: one patch per rank) on the loopback
+    contexts of one GPU, at the FULL radial extent and physics of C5 (manufactured,
+    Ra = 1e5, dt = 1e-4, chi = 16) on a reduced 14 x 40 angular grid, against the
+    oracle: the first step element by element with equal Schwarz counts."""
+    from paper_1905_02300_b200 import Shell
+    full = W.config("C5", G=G)
+    cfg = W.small("C5", full.nr, 14, 40)
+    wl = W.make_workload(cfg)
+    args = (cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt)
+    nslab = G // 2
+    group = Shell.pair(*args, chi=cfg.chi) if nslab == 1 else Shell.slabs(*args, nslab=nslab, chi=cfg.chi)
+    for sh in group:
+        sh.load_workload(wl)
+    o = Oracle(*args, chi=cfg.chi)
+    o.load_workload(wl)
+    group[0].step(1, cfg.tol)
+    o.step(1, cfg.tol)
+    assert all(sh.stats()[-1] == group[0].stats()[-1] for sh in group)
+    assert group[0].stats()[-1][0] == o.stats[-1][0], (group[0].stats(), o.stats)
+    for p in range(2):
+        for s in (1, 2):
+            b = _assemble(group, p, 0, s)
+            c = o.get_fields(p, 0, s)
+            vmax = max(np.max(np.abs(c[q])) for q in ("ur", "ut", "up"))
+            for k in c:
+                assert not np.isnan(b[k]).any(), (p, s, k)
+                den = vmax if k in ("ur", "ut", "up") else max(np.max(np.abs(c[k])), 1e-300)
+                assert np.max(np.abs(b[k] - c[k])) / den <= 1e-11, (G, p, s, k)
