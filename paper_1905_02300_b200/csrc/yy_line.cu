@@ -911,14 +911,15 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
 // patch-folded r), box = one tile (NL lines x n rows along AX)
 inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, int K, int npatch, int AX, int NL,
                             int n) {
-  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-  if (!enc) {
+  // resolved once (thread-safe static initialisation); no libcuda link dependency
+  static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-      return false;
-    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)NPk(g, K), (cuuint64_t)NTk(g, K), (cuuint64_t)NRk(g, K) * npatch};
   const cuuint64_t strides[2] = {(cuuint64_t)NPk(g, K) * 8, (cuuint64_t)NTk(g, K) * NPk(g, K) * 8};
   const cuuint32_t box[3] = {(cuuint32_t)NL, (cuuint32_t)(AX == 1 ? n : 1), (cuuint32_t)(AX == 0 ? n : 1)};
