@@ -11,8 +11,9 @@ over O(1) time: the paper measures at T_f = 10.
 * fast (default, ~2 min): T_f = 2, dt = 0.01 / 0.005 / 0.0025 — system 1 (u1,
   p1 modulo its mean) is first order, and the bootstrapped system 2 (u2, p2) is
   at least 10x more accurate than system 1 at the finest pair;
-* slow (YY_SLOW=1, ~8 min): T_f = 4, dt = 0.005 / 0.0025 / 0.00125 — the
-  second-order slopes of u2, p2 and T (measured 2.16-2.25) and ~1 of u1, p1.
+* slow (YY_SLOW=1, ~13 min): the paper's T_f = 10, dt = 0.005 / 0.0025 /
+  0.00125 — the second-order slopes of u2, p2 (mod mean) and T, measured
+  2.09-2.13 and 2.06 (T_f = 4: 2.16-2.25, profiles/r02_time_order_chi10_tf4.txt).
 """
 import os
 from concurrent.futures import ProcessPoolExecutor
@@ -44,12 +45,14 @@ def test_time_order_system1_first_and_bootstrap_gain():
         assert err[(2, f)][-1] * 10 <= err[(1, f)][-1], (f, err[(2, f)], err[(1, f)])
 
 
-@pytest.mark.skipif(os.environ.get("YY_SLOW") != "1", reason="slow oracle study (YY_SLOW=1)")
-def test_time_order_second_order_after_the_transient():
-    err = _study(4.0, (0.005, 0.0025, 0.00125), 1e-10)
+@pytest.mark.skipif(os.environ.get("YY_SLOW") != "1", reason="slow oracle study (YY_SLOW=1, ~13 min)")
+def test_time_order_second_order_at_the_papers_final_time():
+    # the paper's protocol: errors at T_f = 10; measured on this grid
+    # u2 / p2 (mod mean) / T slopes 2.09-2.13, 2.06 (profiles/r02_time_order_chi10_tf10.txt)
+    err = _study(10.0, (0.005, 0.0025, 0.00125), 1e-10)
     for f in ("ur", "ut", "up", "p~", "T"):
         s2 = _slope(err[(2, f)])[-1]
-        assert 1.8 <= s2 <= 2.3, (f, s2)
+        assert 1.8 <= s2 <= 2.2, (f, s2)
     for f in ("ur", "ut", "up", "p~"):
-        s1 = _slope(err[(1, f)])[-1]
-        assert 0.6 <= s1 <= 1.25, (f, s1)
+        assert _slope(err[(1, f)])[-1] <= 1.25, f          # system 1: at most first order
+        assert err[(2, f)][-1] * 2 <= err[(1, f)][-1], f
