@@ -338,6 +338,31 @@ def test_set_fields_system0_is_both_systems():
                 assert np.array_equal(fa[k], fb[k]), (p, s, k)
 
 
+def test_set_fields_system0_on_a_user_stream_from_pageable_memory():
+    """The uploads (pageable numpy arrays) and system 2's device copies run on the
+    context's stream — a non-blocking torch stream here — and the call returns
+    only when they are done: system 2 equals the host data right away, also after
+    a step has queued kernels on that stream, and so do repeated wall re-sets."""
+    import torch
+    cfg = W.small("C3", 6, 14, 33)
+    st = torch.cuda.Stream()
+    sh = _shell(cfg, stream=st.cuda_stream)
+    wl = W.random_state(cfg, seed=9, amp=2.0)
+    sh.load_workload(wl)
+    sh.step(1, cfg.tol)                       # kernels queued on the user stream
+    for rep in range(3):
+        for p, pd in enumerate(wl["patches"]):
+            n = pd["n"]
+            host = {k: np.array(n[k], copy=True) + rep for k in ("ur", "ut", "up", "T")}
+            host["p"] = np.array(n["p1"], copy=True) - rep
+            sh.set_fields(p, 0, 0, **host)
+            f = sh.get_fields(p, 0, 2)
+            for k in ("ur", "ut", "up", "p"):
+                assert np.array_equal(f[k], host[k]), (rep, p, k)
+            sh.set_wall(p, pd["walls"])       # re-set: the slot buffers are reused
+    sh.step(1, cfg.tol)
+
+
 def test_errors_are_reported():
     from paper_1905_02300_b200 import YYError
     cfg = W.small("C1", 4, 12, 28)

@@ -33,7 +33,7 @@ def run_level(args):
     cfg = W.small("C1", *grid, Ra=1.0, dt=dt, extra={"amp": amp}, R1=R1, R2=R2)
     kw = {}
     if variant:
-        kw["variant"] = variant
+        kw["advection"] = variant          # "split" (the paper's scheme) or "imex"
     if flux:
         kw["flux_fix_eps"] = flux
     o = Oracle(cfg.nr, cfg.nth, cfg.nph, cfg.R1, cfg.R2, cfg.Pr, cfg.Ra, cfg.dt, chi=chi, **kw)
@@ -84,7 +84,7 @@ def main():
     ap.add_argument("--R1", type=float, default=1.0)
     ap.add_argument("--R2", type=float, default=2.0)
     ap.add_argument("--tol", type=float, default=1e-10)
-    ap.add_argument("--variant", default="")
+    ap.add_argument("--variant", default="", help="advection: split (default) | imex")
     ap.add_argument("--flux", type=float, default=0.0, help="mass-flux correction eps (Alg. 1 step 4); 0 = off")
     a = ap.parse_args()
     dts = [float(x) for x in a.dts.split(",")]
