@@ -59,13 +59,19 @@ def main():
              "(dominant kernel) | Oracle cell-updates/s (cores) | Parity max rel err (step 1 / last golden step) | "
              "Iteration counts equal? |",
              "|---|---|---|---|---|---|---|---|---|"]
-    for cfg, label in (("C1", "C1 16×16×48"), ("C2", "C2 48×64×192"), ("C3", "C3 96×128×384"),
-                       ("C5", "C5 (N = 1: 2 × 64×192×576)")):
-        lines.append(row(cfg, label, load(f"r02_bench_{cfg.lower()}.json"), parity, traffic))
-    c4 = load("r01_c4_kernels_v53.json")
+    for cfg, tag, label in (("C1", "c1", "C1 16×16×48"), ("C2", "c2", "C2 48×64×192"),
+                            ("C2", "c2_200", "C2, all 200 BASELINE steps"),
+                            ("C3", "c3", "C3 96×128×384"), ("C3", "c3_100", "C3, all 100 BASELINE steps"),
+                            ("C5", "c5", "C5 (N = 1: 2 × 64×192×576)"), ("C5", "c5_50", "C5, all 50 BASELINE steps"),
+                            ("C5", "c5_k10", "C5, fixed K = 10 (P:L634)")):
+        lines.append(row(cfg, label, load(f"r02_bench_{tag}.json"), parity, traffic))
+    c4 = load("r02_c4_kernels.json")
     if c4:
-        lines.append(f"| C4 (r / θ / φ, kernel only) | 1 | n/a | see `profiles/r01_c4_kernels_v53.json` | — | — | — | "
-                     f"every line of every axis (`test_c4_line_solves_full_size`) | n/a |")
+        ax = c4["axes"]
+        lines.append("| C4 256×384×1152 (kernel only, one sweep per axis) | 1 | n/a | r / θ / φ: "
+                     + " / ".join(f"{ax[a]['ms']:.2f} ms ({ax[a]['GBps'] / 1e3:.2f} TB/s)" for a in ("r", "theta", "phi"))
+                     + " | " + " / ".join(f"{100 * ax[a]['GBps'] / 8000:.0f} %" for a in ("r", "theta", "phi"))
+                     + " of 24 B/elem | — | — | every line of every axis (`test_c4_line_solves_full_size`) | n/a |")
     table = "\n".join(lines)
     path = os.path.join(ROOT, "BASELINE.md")
     s = open(path).read()
