@@ -82,6 +82,7 @@ struct yy_ctx {
   bool heat_only = false;      // eq:HeatDouglas alone (u = 0, no momentum / pressure)
   double flux_eps = 0.0;       // > 0: Algorithm 1 step 4 with this penalty eps
   double* bsplit[4][3] = {};   // split-row tables (Geo::bsplit)
+  double* tsplit[4][3] = {};   // factor-row tables (Geo::tsplit)
   double* adv[4][3] = {};      // per-step transport-velocity row weights (Geo::adv)
   const double* line_a[3] = {};   // a* of the last yy_line_prepare
   double* react_t = nullptr;   // Astar::rt, Astar::rp (per step)
@@ -1376,10 +1377,12 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   ctx->rank = patch0 * nslab + slab;
   for (int q = 0; q < 4; ++q)
     for (int ax = 0; ax < 3; ++ax) {
-      if ((s = dalloc(ctx, &ctx->bsplit[q][ax], (size_t)3 * NRk(g, q) * NTk(g, q))) != YY_OK) { yy_destroy(ctx); return s; }
+      if ((s = dalloc(ctx, &ctx->bsplit[q][ax], (size_t)3 * NRk(g, q) * NTk(g, q))) != YY_OK ||
+          (s = dalloc(ctx, &ctx->tsplit[q][ax], (size_t)3 * NRk(g, q) * NTk(g, q))) != YY_OK) { yy_destroy(ctx); return s; }
       g.bsplit[q][ax] = ctx->bsplit[q][ax];
+      g.tsplit[q][ax] = ctx->tsplit[q][ax];
     }
-  launch_build_split(g, ctx->bsplit, ctx->st);
+  launch_build_split(g, ctx->bsplit, ctx->tsplit, ctx->st);
   for (int K = 0; K < 4; ++K)
     for (int ax = 0; ax < 3; ++ax) {
       if ((s = dalloc(ctx, &ctx->adv[K][ax], npatch * psize(g, K))) != YY_OK) { yy_destroy(ctx); return s; }
@@ -1606,7 +1609,7 @@ yy_status yy_set_param(yy_ctx* ctx, int32_t key, double v) {
       ctx->chi = v;
       ctx->g.cchi = 1.0 / (2.0 * v);
       ctx->g.inv_chi = 1.0 / v;
-      launch_build_split(ctx->g, ctx->bsplit, ctx->st);   // the D_ii rows carry c_chi
+      launch_build_split(ctx->g, ctx->bsplit, ctx->tsplit, ctx->st);   // the D_ii rows carry c_chi
       CK(cudaStreamSynchronize(ctx->st));
       return YY_OK;
     case YY_MAX_ITERS:

@@ -50,6 +50,11 @@ struct Geo {
   // [i][j][am, a0, ap] over the kind's (r, theta) nodes (k-independent), built once
   // on the device from coef<Q, AX, true, false> (yy_kernels.cu: k_build_split)
   const double* bsplit[4][3];
+  // the same rows as the factor rows of I - tau/2 A without the transport /
+  // reaction terms, [i][j][lo0, b0, up0] = (-tau/2 am, 1 - tau/2 a0, -tau/2 ap) of
+  // coef<Q, AX, true, false> (the one-line-per-thread r / theta sweeps: a row is
+  // lo0 - tau/2 adv, b0 + tau/2 rx, up0 + tau/2 adv)
+  const double* tsplit[4][3];
   // per-step transport-velocity row weights by node kind and axis (k_adv; Astar::av)
   const double* adv[4][3];
 };

@@ -199,8 +199,9 @@ void launch_fringe_unpack(const Geo& g, const InterpArgs& a, const double* buf, 
 // out[2 + 2 slot + p] <- sum over slabs s (fixed order) of gath[p * nslab + s][2 + 2 slot + p]
 // (gath: every context's sums, world = 2 nslab contexts ordered rank = patch nslab + slab)
 void launch_flux_fix(const Geo& g, const FluxArgs& a, cudaStream_t st);
-// fill the split-row tables dst[Q][AX] (Geo::bsplit; 3 NRk NTk doubles each)
-void launch_build_split(const Geo& g, double* const (&dst)[4][3], cudaStream_t st);
+// fill the split-row tables dst[Q][AX] (Geo::bsplit; 3 NRk NTk doubles each) and
+// the factor-row tables tdst[Q][AX] (Geo::tsplit, the same size)
+void launch_build_split(const Geo& g, double* const (&dst)[4][3], double* const (&tdst)[4][3], cudaStream_t st);
 void launch_merge_all(double* out, const double* gath, int nslab, cudaStream_t st);
 // slab r-sweeps: solve the 2 nslab boundary system of every line, then x = x0 + xlo X_LO + xhi X_HI
 void launch_slab_solve(const SlabArgs& a, cudaStream_t st);

@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(512) k_flux_fix(Geo g, FluxArgs a) {
 // from the same coef<> the full rows use (Geo::bsplit; rebuilt when chi changes)
 // ---------------------------------------------------------------------------------
 template <int Q, int AX>
-__global__ void k_build_split(Geo g, double* __restrict__ out) {
+__global__ void k_build_split(Geo g, double* __restrict__ out, double* __restrict__ tout) {
   constexpr int K = kind_of(Q);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= NRk(g, K) * NTk(g, K)) return;
@@ -631,6 +631,10 @@ __global__ void k_build_split(Geo g, double* __restrict__ out) {
   out[3 * q] = am;
   out[3 * q + 1] = a0;
   out[3 * q + 2] = ap;
+  const double th = 0.5 * g.tau;     // Geo::tsplit: the factor rows of I - tau/2 A
+  tout[3 * q] = -th * am;
+  tout[3 * q + 1] = 1.0 - th * a0;
+  tout[3 * q + 2] = -th * ap;
 }
 
 // ---------------------------------------------------------------------------------
@@ -828,19 +832,19 @@ void launch_flux_fix(const Geo& g, const FluxArgs& a, cudaStream_t st) {
 }
 
 template <int Q>
-static void build_split_q(const Geo& g, double* const (&dst)[3], cudaStream_t st) {
+static void build_split_q(const Geo& g, double* const (&dst)[3], double* const (&tdst)[3], cudaStream_t st) {
   constexpr int K = kind_of(Q);
   const int n = NRk(g, K) * NTk(g, K), b = (n + 127) / 128;
-  k_build_split<Q, 0><<<b, 128, 0, st>>>(g, dst[0]);
-  k_build_split<Q, 1><<<b, 128, 0, st>>>(g, dst[1]);
-  k_build_split<Q, 2><<<b, 128, 0, st>>>(g, dst[2]);
+  k_build_split<Q, 0><<<b, 128, 0, st>>>(g, dst[0], tdst[0]);
+  k_build_split<Q, 1><<<b, 128, 0, st>>>(g, dst[1], tdst[1]);
+  k_build_split<Q, 2><<<b, 128, 0, st>>>(g, dst[2], tdst[2]);
 }
 
-void launch_build_split(const Geo& g, double* const (&dst)[4][3], cudaStream_t st) {
-  build_split_q<QT>(g, dst[0], st);
-  build_split_q<QUR>(g, dst[1], st);
-  build_split_q<QUT>(g, dst[2], st);
-  build_split_q<QUP>(g, dst[3], st);
+void launch_build_split(const Geo& g, double* const (&dst)[4][3], double* const (&tdst)[4][3], cudaStream_t st) {
+  build_split_q<QT>(g, dst[0], tdst[0], st);
+  build_split_q<QUR>(g, dst[1], tdst[1], st);
+  build_split_q<QUT>(g, dst[2], tdst[2], st);
+  build_split_q<QUP>(g, dst[3], tdst[3], st);
 }
 
 void launch_adv(const Geo& g, const double* ar, const double* at, const double* ap, double* const (&dst)[4][3],

@@ -907,6 +907,283 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------------
+// r and theta sweeps, one line per thread (Thomas), in place in shared memory.
+// A block is ONE warp and owns 32 consecutive k-lines of one (j | i, patch): the
+// tile's inputs arrive by cp.async.bulk.tensor as [row][line] boxes (256-B rows)
+// in TH_RC-row chunks (one mbarrier each, so the elimination starts on the first
+// chunk while the others are in flight); lane k eliminates its line top-down,
+// overwriting the right-hand side with d' and the row weight with c', then
+// back-substitutes bottom-up, x over d'; the result leaves by one bulk tensor
+// store.  FINAL: psi + x goes straight to global memory (coalesced 256-B rows),
+// psi read one row group ahead from L2, where a bulk tensor prefetch put the box
+// at the start.  Per element one reciprocal, no shuffles, no chunk algebra: the
+// instruction count of the partitioned k_line (~135 per element, profiles/
+// r02_ncu.md) drops to the row build (one folded table row, Geo::tsplit) +
+// Thomas.  The phi-fringe lanes (k = 0, nphi - 1) and lanes past the array
+// compute but never store (their rhs goes back unchanged).  Eligible: kinds with
+// an even phi pitch (16-B box origins), n <= 256.
+// ---------------------------------------------------------------------------------
+constexpr int TH_RC = 32;         // rows per load chunk (box rows)
+// rows from the staged factor-row table (Geo::tsplit) or from coef_split: measured
+// on B200 (C3), the plain r-rows of T / u_theta / u_phi (1-D factors, L1 hits)
+// are faster from coef_split, every other row from the table
+__host__ __device__ constexpr bool th_tab(int Q, int AX) { return !(AX == 0 && Q != QUR); }
+// r / theta sweeps that run one line per thread: measured on B200 (C3) every
+// eligible one except the u_theta theta final factor (three staged arrays: two
+// blocks per SM), which keeps k_line_tma
+__host__ __device__ constexpr bool th_route(int Q, int AX, int MODE) {
+  return AX != 2 && (MODE == 0 || MODE == 2) && !(Q == QUT && AX == 1 && MODE == 2);
+}
+constexpr int TH_G = 8;           // rows per elimination group (ILP across the group)
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+               ::"l"(map), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+template <int Q, int AX, int MODE>
+__global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid_constant__ TmaMaps maps) {
+  static_assert(AX != 2 && (MODE == MODE_PLAIN || MODE == MODE_FINAL), "r / theta plain or final sweeps");
+  const uint3 B = bidx(a.rev);
+  constexpr bool FINAL = (MODE == MODE_FINAL);
+  constexpr bool RXR = (Q == QUT && AX == 1);
+  constexpr int K = kind_of(Q);
+  constexpr int G = TH_G;
+  constexpr bool TAB = th_tab(Q, AX);
+  const int patch = B.z;
+  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
+  const int nch = (n + TH_RC - 1) / TH_RC;
+  const int NPAD = nch * TH_RC;
+  const int SA = NPAD * 32;                           // one staged array (doubles)
+  extern __shared__ __align__(128) double sm[];
+  double* Sd = sm;                                    // rhs -> d' -> x
+  double* Sc = Sd + SA;                               // Astar::av -> c'
+  double* Sx = Sc + SA;                               // u_theta reaction (RXR)
+  __shared__ __align__(8) uint64_t bar[8];            // <= 8 chunks
+  const int lane = threadIdx.x;
+  const int k0 = B.x * 32;                            // even: 16-B box origin
+  const int k = k0 + lane;
+  const bool valid = k >= 1 && k <= NPk(g, K) - 2;
+  const int kk = min(max(k, 1), NPk(g, K) - 2);
+  int i0, j0;
+  if (AX == 0) { i0 = i_lo<K>(g); j0 = B.y + 1; }
+  else { i0 = B.y + i_lo<K>(g); j0 = 1; }
+  const int c1 = j0, c2 = patch * NRk(g, K) + i0;
+  // rows of this lane's line: element m at Rl + m rs (Rl clamped to a valid node)
+  const int rs = (AX == 0) ? SR<K>(g) : ST<K>(g);
+  const long long lofs = patch * psize(g, K) + IX<K>(g, i0, j0, kk);
+  if (lane == 0) {
+    for (int c = 0; c < nch; ++c)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[c])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // IMEX (noadv): the rows carry no transport terms, only the rhs is staged
+    const int NIN = a.noadv ? 1 : 2 + (RXR ? 1 : 0);
+    const uint32_t cb = (uint32_t)(TH_RC * 32 * sizeof(double));
+    for (int c = 0; c < nch; ++c) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[c])), "r"(NIN * cb)
+                   : "memory");
+      const int o = c * TH_RC * 32;
+      const int r1 = AX == 1 ? c1 + c * TH_RC : c1, r2 = AX == 0 ? c2 + c * TH_RC : c2;
+      tma_load_3d(Sd + o, &maps.m[0], &bar[c], k0, r1, r2);
+      if (!a.noadv) {
+        tma_load_3d(Sc + o, &maps.m[1], &bar[c], k0, r1, r2);
+        if (RXR) tma_load_3d(Sx + o, &maps.m[2], &bar[c], k0, r1, r2);
+      }
+    }
+    if (FINAL) tma_prefetch_3d(&maps.m[3], k0, c1, c2);
+  }
+  __syncwarp();
+  const double th = 0.5 * g.tau;
+  auto wait = [&](int c) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n"
+        ::"r"(smem_u32(&bar[c])) : "memory");
+  };
+  // Forward elimination of the raw rows  a_m x_{m-1} + b_m x_m + c_m x_{m+1} = d_m
+  // through the continuants (leading principal minors)
+  //     q_m = b_m q_{m-1} - a_m c_{m-1} q_{m-2},   q_{-1} = 1, q_{-2} = 0,
+  // whose ratios are the Thomas pivots (b_m - a_m c'_{m-1} = q_m / q_{m-1}): the
+  // serial chain is one fma per row, the reciprocals of the pivots are independent
+  // of each other (ILP across the G rows of a group), and so is the d' recurrence
+  // d'_m = d_m/piv_m - (a_m/piv_m) d'_{m-1} (one fma per row).  The continuants are
+  // rescaled by a power of two after every group (exact; no overflow for any tau).
+  // Row 0's lower weight meets c_{-1} = q_{-2} = d'_{-1} = 0 and needs no mask;
+  // the group holding row n-1 (line end: c = 0, wall ghost) and the padding rows
+  // past n (identity rows) takes the masked build (EDGE), like the first group of a
+  // wall line.
+  double qm1 = 1.0, qm2 = 0.0, cprev = 0.0, dp = 0.0;
+  // the factor-row table of this tile's lines (Geo::tsplit rows i0.., j0..) into
+  // shared memory (TAB), or the rows from coef_split and the 1-D factors
+  double* St = Sx + (RXR ? SA : 0);
+  if (TAB) {
+    // (all of a lane's loads in flight at once: <= 3 * 256 / 32 = 24 per lane; the
+    // latency overlaps the first chunk's)
+    const double* __restrict__ T3 = g.tsplit[Q][AX] + 3 * (i0 * NTk(g, K) + j0);
+    const int tstride = (AX == 0) ? 3 * NTk(g, K) : 3;
+    double tv[24];
+#pragma unroll
+    for (int t = 0; t < 24; ++t) {
+      const int e = min(lane + 32 * t, 3 * n - 1);
+      tv[t] = __ldg(T3 + (e / 3) * tstride + e % 3);
+    }
+#pragma unroll
+    for (int t = 0; t < 24; ++t)
+      if (lane + 32 * t < 3 * n) St[lane + 32 * t] = tv[t];
+    __syncwarp();
+  }
+  const Astar Az{nullptr, nullptr, nullptr, nullptr, nullptr};
+  auto group = [&](int m0, auto edge, auto noadv) {
+    constexpr bool EDGE = decltype(edge)::value, NOADV = decltype(noadv)::value;
+    double ra[G], rb[G], rc[G], rd[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int m = m0 + u, mm = EDGE ? min(m, n - 1) : m;
+      const int q = m * 32 + lane;
+      double lo, bm, up;
+      if (TAB) {
+        // the row's a*-independent part from Geo::tsplit (staged in shared memory:
+        // a broadcast read), the transport weight Astar::av and the u_theta
+        // reaction from the tile
+        lo = St[3 * mm];
+        bm = St[3 * mm + 1];
+        up = St[3 * mm + 2];
+        if (!NOADV) {
+          const double adv = Sc[q];
+          lo = fma(-th, adv, lo);
+          up = fma(th, adv, up);
+          if (RXR) bm = fma(th, Sx[q], bm);
+        }
+      } else {
+        const int i = (AX == 0) ? i0 + mm : i0, j = (AX == 0) ? j0 : j0 + mm;
+        double am, a0, ap;
+        coef_split<Q, AX, RX_GIVEN>(g, Az, i, j, kk, am, a0, ap, NOADV ? 0.0 : Sc[q],
+                                    (RXR && !NOADV) ? Sx[q] : 0.0);
+        bm = 1.0 - th * a0;
+        lo = -th * am;
+        up = -th * ap;
+      }
+      double rv = Sd[q];
+      if (EDGE) {
+        if (AX == 0 && K != KR) {      // antisymmetric wall ghost of the increment (RD23)
+          if (m == 0 && g.wall_lo) bm -= lo;
+          if (m == n - 1 && g.wall_hi) bm -= up;
+        }
+        if (m >= n - 1) up = 0.0;      // line end: homogeneous Dirichlet increment
+        if (m >= n) { lo = 0.0; bm = 1.0; rv = 0.0; }
+      }
+      ra[u] = lo; rb[u] = bm; rc[u] = up; rd[u] = rv;
+    }
+    double qv[G];
+    const double q0 = qm1;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const double e = ra[u] * (u ? rc[u - 1] : cprev);
+      const double qn = fma(rb[u], qm1, -(e * qm2));
+      qv[u] = qn;
+      qm2 = qm1;
+      qm1 = qn;
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int q = (m0 + u) * 32 + lane;
+      const double inv = (u ? qv[u - 1] : q0) * frcp(qv[u]);
+      dp = fma(-(ra[u] * inv), dp, rd[u] * inv);
+      if (valid) {
+        Sc[q] = rc[u] * inv;
+        Sd[q] = dp;
+      }
+    }
+    cprev = rc[G - 1];
+    // 2^-e of q_{m0+G-1} (exact rescaling of the two carried continuants)
+    const long long eb = (__double_as_longlong(qm1) >> 52) & 0x7ff;
+    const double sc = __longlong_as_double((2046LL - eb) << 52);
+    qm1 *= sc;
+    qm2 *= sc;
+  };
+  // (IMEX, noadv: a block-uniform branch outside the unrolled rows)
+  auto forward = [&](auto noadv) {
+    for (int c = 0; c < nch; ++c) {
+      wait(c);
+      for (int m0 = c * TH_RC; m0 < (c + 1) * TH_RC; m0 += G) {
+        const bool edge = m0 + G > n - 1 || (AX == 0 && K != KR && m0 == 0 && g.wall_lo);
+        if (edge) group(m0, std::true_type{}, noadv);
+        else group(m0, std::false_type{}, noadv);
+      }
+    }
+  };
+  if (a.noadv) forward(std::true_type{});
+  else forward(std::false_type{});
+  // back substitution x_m = d'_m - c'_m x_{m+1} from the padded top (x = 0 there:
+  // the padding rows are identity rows with d = 0).  PLAIN: x over d', then one
+  // bulk tensor store.  FINAL: psi + x straight to global (coalesced 256-B rows),
+  // psi loaded one group ahead from L2 (the box was prefetched at the start).
+  constexpr int GB = 16;
+  double x = 0.0;
+  if constexpr (!FINAL) {
+    for (int m0 = NPAD - GB; m0 >= 0; m0 -= GB) {
+      double cv[GB], dv[GB];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int q = (m0 + u) * 32 + lane;
+        cv[u] = Sc[q];
+        dv[u] = Sd[q];
+      }
+#pragma unroll
+      for (int u = GB - 1; u >= 0; --u) {
+        x = fma(-cv[u], x, dv[u]);
+        if (valid) Sd[(m0 + u) * 32 + lane] = x;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&maps.m[3], Sd, k0, c1, c2);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+  } else {
+    double* __restrict__ P = a.psi + lofs;
+    double wsum = 0.0;
+    double pv[GB], pn[GB];
+    // (volatile: issued here, one row group ahead of their use — plain loads were
+    // sunk next to their uses, one L2 round trip per row, profiles/r02_th_ncu.md)
+    auto load_psi = [&](int m0, double (&dst)[GB]) {
+#pragma unroll
+      for (int u = 0; u < GB; ++u)
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(dst[u]) : "l"(P + min(m0 + u, n - 1) * rs));
+    };
+    load_psi(NPAD - GB, pv);
+    for (int m0 = NPAD - GB; m0 >= 0; m0 -= GB) {
+      if (m0 >= GB) load_psi(m0 - GB, pn);
+      double cv[GB], dv[GB];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int q = (m0 + u) * 32 + lane;
+        cv[u] = Sc[q];
+        dv[u] = Sd[q];
+      }
+#pragma unroll
+      for (int u = GB - 1; u >= 0; --u) {
+        const int m = m0 + u;
+        x = fma(-cv[u], x, dv[u]);
+        const int mm = min(m, n - 1);
+        const int i = (AX == 0) ? i0 + mm : i0, j = (AX == 0) ? j0 : j0 + mm;
+        const double r = rnode<K>(g, i), w = r * r * snode<K>(g, j);
+        if (valid && m < n) {
+          P[m * rs] = pv[u] + x;
+          wsum = fma(w * x, x, wsum);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GB; ++u) pv[u] = pn[u];
+    }
+    wsum *= g.dr * g.dth * g.dph;
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_down_sync(FULL, wsum, o);
+    if (lane == 0) a.part[(long long)patch * a.maxb + B.y * gridDim.x + B.x] = wsum;
+  }
+}
+
 // host: a 3-D tensor map over every patch of one kind-K array (dims phi, theta,
 // patch-folded r), box = one tile (NL lines x n rows along AX)
 inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, int K, int npatch, int AX, int NL,
@@ -937,6 +1214,47 @@ inline bool use_tma() {
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
+}
+
+// env YY_THOMAS (default 1): r / theta plain and final sweeps of the TMA-eligible
+// kinds on k_line_th (one line per thread)
+inline bool use_thomas() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("YY_THOMAS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int Q, int AX, int MODE>
+int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
+  constexpr int K = kind_of(Q);
+  constexpr bool FINAL = (MODE == MODE_FINAL);
+  const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
+  const int nch = (n + TH_RC - 1) / TH_RC;
+  // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
+  // kinds loses to k_line, 2.0 vs 3.1 TB/s)
+  if ((NPk(g, K) % 2) || n > 256 || nch > 8) return -1;
+  const size_t smem =
+      ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + (th_tab(Q, AX) ? 3 * n : 0)) * sizeof(double);
+  if (smem > 72 * 1024) return -1;                   // >= 3 blocks per SM (measured: 2 lose)
+  // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (psi
+  // for FINAL, prefetched; PLAIN: the right-hand side array, stored)
+  TmaMaps maps{};
+  bool ok = encode_tile_map(&maps.m[0], a.R, g, K, npatch, AX, 32, TH_RC) &&
+            encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, TH_RC) &&
+            encode_tile_map(&maps.m[3], FINAL ? a.psi : a.R, g, K, npatch, AX, 32, n);
+  if (ok && Q == QUT && AX == 1) ok = encode_tile_map(&maps.m[2], a.rt, g, K, npatch, AX, 32, TH_RC);
+  if (!ok) return -1;
+  static size_t attr = 0;          // the largest opted-in size
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_line_th<Q, AX, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const dim3 grid((NPk(g, K) + 31) / 32, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
+  k_line_th<Q, AX, MODE><<<grid, 32, smem, st>>>(g, a, maps);
+  return (int)(grid.x * grid.y);
 }
 
 template <int Q, int AX, int MODE, int P, int M>
@@ -975,6 +1293,12 @@ template <int Q, int AX, int MODE, int S, int P, int M>
 int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch, cudaStream_t st) {
   // theta sweeps only: measured on B200 (C3) the theta classes gain 3-9 %, the r
   // sweeps lose up to 12 % (their box rows lie 393 KB apart)
+  if constexpr (th_route(Q, AX, MODE) && P <= 32) {
+    if (use_thomas()) {
+      const int nb = launch_th<Q, AX, MODE>(g, a, npatch, st);
+      if (nb >= 0) return nb;
+    }
+  }
   if constexpr (AX == 1 && (MODE == MODE_PLAIN || MODE == MODE_FINAL) && P <= 32 && M <= 8) {
     if (use_tma()) {
       const int nb = launch_tma<Q, AX, MODE, P, M>(g, a, npatch, st);
