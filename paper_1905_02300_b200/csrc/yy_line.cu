@@ -817,12 +817,26 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
     if (FINAL) tma_load_3d(Sps, &maps.m[3], &bar, c0, c1, c2);
   }
   (void)NIN;
+  // the factor-row table of the tile's rows (Geo::tsplit: lo0, b0, up0 per row) and,
+  // FINAL, the norm weights r^2 sin(theta) into shared memory while the boxes are in
+  // flight: the row build reads no global tables (their L2 latency was the largest
+  // stall of this kernel, profiles/r02_ncu.md)
+  double* St = Sps + SA;
+  double* Sw = St + 3 * NPAD;
+  {
+    const double* __restrict__ T3 = g.tsplit[Q][AX] + 3 * (i0 * NTk(g, K) + j0);
+    const int tstride = (AX == 0) ? 3 * NTk(g, K) : 3;
+    for (int e = threadIdx.x; e < 3 * n; e += 128) St[e] = __ldg(T3 + (e / 3) * tstride + e % 3);
+    if (FINAL)
+      for (int m = threadIdx.x; m < n; m += 128) {
+        const int i = (AX == 0) ? i0 + m : i0, j = (AX == 0) ? j0 : j0 + m;
+        const double r = rnode<K>(g, i);
+        Sw[m] = r * r * snode<K>(g, j);
+      }
+  }
   __syncthreads();                                    // the barrier is initialised
-  Astar A{a.ar + patch * psize(g, KR), a.at + patch * psize(g, KT), a.ap + patch * psize(g, KP),
-          a.rt + patch * psize(g, KT), a.rp + patch * psize(g, KP)};
-  bind_adv<K>(g, A, patch);
+  const double th = 0.5 * g.tau;
   const int lt = threadIdx.x % NL, rg = threadIdx.x / NL;   // build / write-back: line, row group
-  const int kk = min(max(k0 + lt, 1), NPk(g, K) - 2);
   auto slot = [&](int l, int e) { return l * LP + (e / M) * MP + (e % M); };
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n"
@@ -842,9 +856,16 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
   for (int u = 0; u < M; ++u) {
     const int e = u * P + rg;
     const int ec = min(e, n - 1);
-    const int i = (AX == 0) ? i0 + ec : i0, j = (AX == 0) ? j0 : j0 + ec;
-    double lo, up, rh;
-    make_row<Q, AX, RX_GIVEN>(g, A, i, j, kk, ec, n, vr[u], lo, up, rh, false, va[u], vx[u]);
+    // the row of make_row from the folded table: raw weights, then normalised by
+    // the diagonal (line ends: homogeneous Dirichlet increments)
+    const double lr = fma(-th, va[u], St[3 * ec]), ur = fma(th, va[u], St[3 * ec + 2]);
+    double bm = fma(th, vx[u], St[3 * ec + 1]);
+    if (AX == 0 && K != KR) {            // antisymmetric wall ghost of the increment (RD23)
+      if (ec == 0 && g.wall_lo) bm -= lr;
+      if (ec == n - 1 && g.wall_hi) bm -= ur;
+    }
+    const double inv = frcp(bm);
+    const double lo = (ec == 0) ? 0.0 : lr * inv, up = (ec == n - 1) ? 0.0 : ur * inv, rh = vr[u] * inv;
     const double mk = (e < n && lvalid(lt)) ? 1.0 : 0.0;
     const int s = slot(lt, e);
     LO[s] = lo * mk;
@@ -881,9 +902,7 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
       const double x = RH[slot(lt, e)];
       if (FINAL) {
         out[q] = Sps[q] + x;
-        const int i = (AX == 0) ? i0 + e : i0, j = (AX == 0) ? j0 : j0 + e;
-        const double r = rnode<K>(g, i), sn = snode<K>(g, j);
-        wsum += r * r * sn * x * x;
+        wsum += Sw[e] * x * x;
       } else {
         out[q] = x;
       }
@@ -1032,6 +1051,16 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
       if (lane + 32 * t < 3 * n) St[lane + 32 * t] = tv[t];
     __syncwarp();
   }
+  // FINAL: the norm weights r^2 sin(theta) of the tile's rows
+  double* Sw = St + (TAB ? 3 * n : 0);
+  if (FINAL) {
+    for (int m = lane; m < n; m += 32) {
+      const int i = (AX == 0) ? i0 + m : i0, j = (AX == 0) ? j0 : j0 + m;
+      const double r = rnode<K>(g, i);
+      Sw[m] = r * r * snode<K>(g, j);
+    }
+    __syncwarp();
+  }
   const Astar Az{nullptr, nullptr, nullptr, nullptr, nullptr};
   auto group = [&](int m0, auto edge, auto noadv) {
     constexpr bool EDGE = decltype(edge)::value, NOADV = decltype(noadv)::value;
@@ -1145,17 +1174,18 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   } else {
     double* __restrict__ P = a.psi + lofs;
     double wsum = 0.0;
-    double pv[GB], pn[GB];
-    // (volatile: issued here, one row group ahead of their use — plain loads were
-    // sunk next to their uses, one L2 round trip per row, profiles/r02_th_ncu.md)
+    // psi of a row group is loaded two groups ahead of its use (ping-pong
+    // registers, no copies; volatile: issued where written — plain loads were sunk
+    // next to their uses), the norm weights r^2 sin(theta) come from Sw
     auto load_psi = [&](int m0, double (&dst)[GB]) {
+      const double* Pm = P + m0 * rs;
 #pragma unroll
-      for (int u = 0; u < GB; ++u)
-        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(dst[u]) : "l"(P + min(m0 + u, n - 1) * rs));
+      for (int u = 0; u < GB; ++u) {
+        const double* pu = (m0 + u < n) ? Pm + u * rs : P;
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(dst[u]) : "l"(pu));
+      }
     };
-    load_psi(NPAD - GB, pv);
-    for (int m0 = NPAD - GB; m0 >= 0; m0 -= GB) {
-      if (m0 >= GB) load_psi(m0 - GB, pn);
+    auto back = [&](int m0, const double (&pv)[GB]) {
       double cv[GB], dv[GB];
 #pragma unroll
       for (int u = 0; u < GB; ++u) {
@@ -1163,20 +1193,23 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
         cv[u] = Sc[q];
         dv[u] = Sd[q];
       }
+      double* Pm = P + m0 * rs;
 #pragma unroll
       for (int u = GB - 1; u >= 0; --u) {
-        const int m = m0 + u;
         x = fma(-cv[u], x, dv[u]);
-        const int mm = min(m, n - 1);
-        const int i = (AX == 0) ? i0 + mm : i0, j = (AX == 0) ? j0 : j0 + mm;
-        const double r = rnode<K>(g, i), w = r * r * snode<K>(g, j);
-        if (valid && m < n) {
-          P[m * rs] = pv[u] + x;
-          wsum = fma(w * x, x, wsum);
+        if (valid && m0 + u < n) {
+          Pm[u * rs] = pv[u] + x;
+          wsum = fma(Sw[m0 + u] * x, x, wsum);
         }
       }
-#pragma unroll
-      for (int u = 0; u < GB; ++u) pv[u] = pn[u];
+    };
+    double pa[GB], pb[GB];
+    load_psi(NPAD - GB, pa);
+    for (int m0 = NPAD - GB; m0 > 0; m0 -= 2 * GB) {   // NPAD is a multiple of 2 GB
+      load_psi(m0 - GB, pb);
+      back(m0, pa);
+      if (m0 >= 2 * GB) load_psi(m0 - 2 * GB, pa);
+      back(m0 - GB, pb);
     }
     wsum *= g.dr * g.dth * g.dph;
     for (int o = 16; o > 0; o >>= 1) wsum += __shfl_down_sync(FULL, wsum, o);
@@ -1236,8 +1269,8 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
   // kinds loses to k_line, 2.0 vs 3.1 TB/s)
   if ((NPk(g, K) % 2) || n > 256 || nch > 8) return -1;
-  const size_t smem =
-      ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + (th_tab(Q, AX) ? 3 * n : 0)) * sizeof(double);
+  const size_t smem = ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + (th_tab(Q, AX) ? 3 * n : 0) +
+                        (FINAL ? n : 0)) * sizeof(double);
   if (smem > 72 * 1024) return -1;                   // >= 3 blocks per SM (measured: 2 lose)
   // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (psi
   // for FINAL, prefetched; PLAIN: the right-hand side array, stored)
@@ -1275,7 +1308,7 @@ int launch_tma(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int NIN = tma_narr<Q, AX, FINAL>() - 1;
   constexpr int TILE = 3 * NL * line_pitch<P, (M | 1)>();
   constexpr int FRONT = (NIN * SA > TILE ? NIN * SA : TILE + 15) / 16 * 16;
-  const size_t smem = ((size_t)FRONT + SA) * sizeof(double);
+  const size_t smem = ((size_t)FRONT + SA + 4 * P * M) * sizeof(double);   // + row table, norm weights
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_line_tma<Q, AX, MODE, P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
