@@ -1260,6 +1260,16 @@ inline bool use_thomas() {
   return v == 1;
 }
 
+// env YY_TH_SMEM (KB, default 110): the largest k_line_th tile
+inline int th_smem_max() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("YY_TH_SMEM");
+    v = e ? atoi(e) : 110;
+  }
+  return v;
+}
+
 template <int Q, int AX, int MODE>
 int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
@@ -1271,7 +1281,9 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   if ((NPk(g, K) % 2) || n > 256 || nch > 8) return -1;
   const size_t smem = ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + (th_tab(Q, AX) ? 3 * n : 0) +
                         (FINAL ? n : 0)) * sizeof(double);
-  if (smem > 72 * 1024) return -1;                   // >= 3 blocks per SM (measured: 2 lose)
+  // measured on B200: two blocks per SM (C5 theta, 96 KB tiles) still beat the
+  // partitioned k_line (3.1-3.3 vs 2.6-2.7 TB/s); one does not
+  if (smem > (size_t)th_smem_max() * 1024) return -1;
   // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (psi
   // for FINAL, prefetched; PLAIN: the right-hand side array, stored)
   TmaMaps maps{};
@@ -1322,6 +1334,9 @@ int launch_tma(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
 // ---------------------------------------------------------------------------------
 // launch: pick (P, M) with P*M >= n
 // ---------------------------------------------------------------------------------
+#ifndef TMA_MMAX
+#define TMA_MMAX 16
+#endif
 template <int Q, int AX, int MODE, int S, int P, int M>
 int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch, cudaStream_t st) {
   // theta sweeps only: measured on B200 (C3) the theta classes gain 3-9 %, the r
@@ -1332,7 +1347,7 @@ int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatc
       if (nb >= 0) return nb;
     }
   }
-  if constexpr (AX == 1 && (MODE == MODE_PLAIN || MODE == MODE_FINAL) && P <= 32 && M <= 8) {
+  if constexpr (AX == 1 && (MODE == MODE_PLAIN || MODE == MODE_FINAL) && P <= 32 && M <= TMA_MMAX) {
     if (use_tma()) {
       const int nb = launch_tma<Q, AX, MODE, P, M>(g, a, npatch, st);
       if (nb >= 0) return nb;
