@@ -17,11 +17,12 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def klass(name):
-    m = re.search(r"k_(line_tma|line|resid|pres)<([^>]*)>", name)
+    m = re.search(r"k_(line_tma|line_th|line|resid|pres)<([^>]*)>", name)
     if not m:
         return None
-    a = [int(re.sub(r"\(int\)", "", x).strip()) for x in m.group(2).split(",")]
-    if m.group(1) == "line_tma":       # k_line_tma<Q, AX, MODE, P, M>
+    a = [int(re.sub(r"\(int\)|\(bool\)", "", x).strip().replace("true", "1").replace("false", "0"))
+         for x in m.group(2).split(",")]
+    if m.group(1) in ("line_tma", "line_th"):   # k_line_tma<Q, AX, MODE, P, M>, k_line_th<Q, AX, MODE>
         return f"sweep_{Q[a[0]]}_{AX[a[1]]}" + ("_fin" if a[2] == 2 else "")
     if m.group(1) == "resid":          # k_resid<Q, S, IB>
         return "resid_" + Q[a[0]] + ("" if a[0] == 0 else str(a[1]))
