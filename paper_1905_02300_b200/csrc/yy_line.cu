@@ -933,10 +933,9 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
 // in TH_RC-row chunks (one mbarrier each, so the elimination starts on the first
 // chunk while the others are in flight); lane k eliminates its line top-down,
 // overwriting the right-hand side with d' and the row weight with c', then
-// back-substitutes bottom-up, x over d'; the result leaves by one bulk tensor
-// store.  FINAL: psi + x goes straight to global memory (coalesced 256-B rows),
-// psi read one row group ahead from L2, where a bulk tensor prefetch put the box
-// at the start.  Per element one reciprocal, no shuffles, no chunk algebra: the
+// back-substitutes bottom-up; x leaves by one bulk tensor store (r) or straight
+// to global memory in coalesced 256-B rows (theta; FINAL: psi + x, psi read two
+// row groups ahead from L2, where a bulk tensor prefetch put the box at the start).  Per element one reciprocal, no shuffles, no chunk algebra: the
 // instruction count of the partitioned k_line (~135 per element, profiles/
 // r02_ncu.md) drops to the row build (one folded table row, Geo::tsplit) +
 // Thomas.  The phi-fringe lanes (k = 0, nphi - 1) and lanes past the array
@@ -1092,16 +1091,23 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
         lo = -th * am;
         up = -th * ap;
       }
-      double rv = Sd[q];
-      if (EDGE) {
-        if (AX == 0 && K != KR) {      // antisymmetric wall ghost of the increment (RD23)
-          if (m == 0 && g.wall_lo) bm -= lo;
-          if (m == n - 1 && g.wall_hi) bm -= up;
+      ra[u] = lo; rb[u] = bm; rc[u] = up; rd[u] = Sd[q];
+    }
+    if (EDGE) {
+      // the line's first row: antisymmetric wall ghost of the increment (RD23);
+      // its last row ul: wall ghost and c = 0 (homogeneous Dirichlet increment);
+      // rows past it (padding): identity rows with d = 0
+      if (AX == 0 && K != KR && m0 == 0 && g.wall_lo) rb[0] -= ra[0];
+      const int ul = n - 1 - m0;
+      const bool gh = AX == 0 && K != KR && g.wall_hi;
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        if (u == ul) {
+          if (gh) rb[u] -= rc[u];
+          rc[u] = 0.0;
         }
-        if (m >= n - 1) up = 0.0;      // line end: homogeneous Dirichlet increment
-        if (m >= n) { lo = 0.0; bm = 1.0; rv = 0.0; }
+        if (u > ul) { ra[u] = 0.0; rb[u] = 1.0; rc[u] = 0.0; rd[u] = 0.0; }
       }
-      ra[u] = lo; rb[u] = bm; rc[u] = up; rd[u] = rv;
     }
     double qv[G];
     const double q0 = qm1;
@@ -1158,18 +1164,28 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
         cv[u] = Sc[q];
         dv[u] = Sd[q];
       }
+      // theta: x straight to global memory (coalesced 256-B rows, no bulk store to
+      // wait for before the block exits); r: x over d', then one bulk tensor store
+      // (measured on B200: each the faster for its axis)
+      double* __restrict__ Rm = a.R + lofs + (long long)m0 * rs;
 #pragma unroll
       for (int u = GB - 1; u >= 0; --u) {
         x = fma(-cv[u], x, dv[u]);
-        if (valid) Sd[(m0 + u) * 32 + lane] = x;
+        if (AX == 1) {
+          if (valid && m0 + u < n) Rm[u * rs] = x;
+        } else if (valid) {
+          Sd[(m0 + u) * 32 + lane] = x;
+        }
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_3d(&maps.m[3], Sd, k0, c1, c2);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (AX == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&maps.m[3], Sd, k0, c1, c2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
     }
   } else {
     double* __restrict__ P = a.psi + lofs;
@@ -1284,12 +1300,12 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   // measured on B200: two blocks per SM (C5 theta, 96 KB tiles) still beat the
   // partitioned k_line (3.1-3.3 vs 2.6-2.7 TB/s); one does not
   if (smem > (size_t)th_smem_max() * 1024) return -1;
-  // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (psi
-  // for FINAL, prefetched; PLAIN: the right-hand side array, stored)
+  // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (FINAL:
+  // psi, prefetched into L2; PLAIN r: the right-hand side array, stored)
   TmaMaps maps{};
   bool ok = encode_tile_map(&maps.m[0], a.R, g, K, npatch, AX, 32, TH_RC) &&
-            encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, TH_RC) &&
-            encode_tile_map(&maps.m[3], FINAL ? a.psi : a.R, g, K, npatch, AX, 32, n);
+            encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, TH_RC);
+  if (ok && (FINAL || AX == 0)) ok = encode_tile_map(&maps.m[3], FINAL ? a.psi : a.R, g, K, npatch, AX, 32, n);
   if (ok && Q == QUT && AX == 1) ok = encode_tile_map(&maps.m[2], a.rt, g, K, npatch, AX, 32, TH_RC);
   if (!ok) return -1;
   static size_t attr = 0;          // the largest opted-in size
