@@ -943,17 +943,19 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
 // an even phi pitch (16-B box origins), n <= 256.
 // ---------------------------------------------------------------------------------
 constexpr int TH_RC = 32;         // rows per load chunk (box rows)
-// rows from the staged factor-row table (Geo::tsplit) or from coef_split: measured
-// on B200 (C3), the plain r-rows of T / u_theta / u_phi (1-D factors, L1 hits)
-// are faster from coef_split, every other row from the table
-__host__ __device__ constexpr bool th_tab(int Q, int AX) { return !(AX == 0 && Q != QUR); }
+
 // r / theta sweeps that run one line per thread: measured on B200 (C3) every
 // eligible one except the u_theta theta final factor (three staged arrays: two
 // blocks per SM), which keeps k_line_tma
 __host__ __device__ constexpr bool th_route(int Q, int AX, int MODE) {
   return AX != 2 && (MODE == 0 || MODE == 2) && !(Q == QUT && AX == 1 && MODE == 2);
 }
-constexpr int TH_G = 8;           // rows per elimination group (ILP across the group)
+#ifndef YY_TH_G
+#define YY_TH_G 16
+#endif
+// rows per elimination group (ILP across the group; measured on B200: 16 beats 8
+// by 3-5 %, 4 loses 8 %, 32 spills)
+constexpr int TH_G = YY_TH_G;
 
 __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
@@ -968,7 +970,6 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   constexpr bool RXR = (Q == QUT && AX == 1);
   constexpr int K = kind_of(Q);
   constexpr int G = TH_G;
-  constexpr bool TAB = th_tab(Q, AX);
   const int patch = B.z;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
   const int nch = (n + TH_RC - 1) / TH_RC;
@@ -1032,9 +1033,10 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   // wall line.
   double qm1 = 1.0, qm2 = 0.0, cprev = 0.0, dp = 0.0;
   // the factor-row table of this tile's lines (Geo::tsplit rows i0.., j0..) into
-  // shared memory (TAB), or the rows from coef_split and the 1-D factors
+  // shared memory (measured on B200: on a par with coef_split's 1-D factor loads
+  // for the plain r-rows, 3-5 % faster for the rest)
   double* St = Sx + (RXR ? SA : 0);
-  if (TAB) {
+  {
     // (all of a lane's loads in flight at once: <= 3 * 256 / 32 = 24 per lane; the
     // latency overlaps the first chunk's)
     const double* __restrict__ T3 = g.tsplit[Q][AX] + 3 * (i0 * NTk(g, K) + j0);
@@ -1051,7 +1053,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     __syncwarp();
   }
   // FINAL: the norm weights r^2 sin(theta) of the tile's rows
-  double* Sw = St + (TAB ? 3 * n : 0);
+  double* Sw = St + 3 * n;
   if (FINAL) {
     for (int m = lane; m < n; m += 32) {
       const int i = (AX == 0) ? i0 + m : i0, j = (AX == 0) ? j0 : j0 + m;
@@ -1060,7 +1062,6 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     }
     __syncwarp();
   }
-  const Astar Az{nullptr, nullptr, nullptr, nullptr, nullptr};
   auto group = [&](int m0, auto edge, auto noadv) {
     constexpr bool EDGE = decltype(edge)::value, NOADV = decltype(noadv)::value;
     double ra[G], rb[G], rc[G], rd[G];
@@ -1068,28 +1069,14 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     for (int u = 0; u < G; ++u) {
       const int m = m0 + u, mm = EDGE ? min(m, n - 1) : m;
       const int q = m * 32 + lane;
-      double lo, bm, up;
-      if (TAB) {
-        // the row's a*-independent part from Geo::tsplit (staged in shared memory:
-        // a broadcast read), the transport weight Astar::av and the u_theta
-        // reaction from the tile
-        lo = St[3 * mm];
-        bm = St[3 * mm + 1];
-        up = St[3 * mm + 2];
-        if (!NOADV) {
-          const double adv = Sc[q];
-          lo = fma(-th, adv, lo);
-          up = fma(th, adv, up);
-          if (RXR) bm = fma(th, Sx[q], bm);
-        }
-      } else {
-        const int i = (AX == 0) ? i0 + mm : i0, j = (AX == 0) ? j0 : j0 + mm;
-        double am, a0, ap;
-        coef_split<Q, AX, RX_GIVEN>(g, Az, i, j, kk, am, a0, ap, NOADV ? 0.0 : Sc[q],
-                                    (RXR && !NOADV) ? Sx[q] : 0.0);
-        bm = 1.0 - th * a0;
-        lo = -th * am;
-        up = -th * ap;
+      // the row's a*-independent part from Geo::tsplit (staged: a broadcast read),
+      // the transport weight Astar::av and the u_theta reaction from the tile
+      double lo = St[3 * mm], bm = St[3 * mm + 1], up = St[3 * mm + 2];
+      if (!NOADV) {
+        const double adv = Sc[q];
+        lo = fma(-th, adv, lo);
+        up = fma(th, adv, up);
+        if (RXR) bm = fma(th, Sx[q], bm);
       }
       ra[u] = lo; rb[u] = bm; rc[u] = up; rd[u] = Sd[q];
     }
@@ -1295,8 +1282,8 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
   // kinds loses to k_line, 2.0 vs 3.1 TB/s)
   if ((NPk(g, K) % 2) || n > 256 || nch > 8) return -1;
-  const size_t smem = ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + (th_tab(Q, AX) ? 3 * n : 0) +
-                        (FINAL ? n : 0)) * sizeof(double);
+  const size_t smem =
+      ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + 3 * n + (FINAL ? n : 0)) * sizeof(double);
   // measured on B200: two blocks per SM (C5 theta, 96 KB tiles) still beat the
   // partitioned k_line (3.1-3.3 vs 2.6-2.7 TB/s); one does not
   if (smem > (size_t)th_smem_max() * 1024) return -1;
