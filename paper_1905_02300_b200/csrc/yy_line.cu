@@ -50,7 +50,7 @@
 #define YY_IMEX_FAST 1   // IMEX rows without the per-step weight reads (0: IMEX reads the zero arrays)
 #endif
 #ifndef YY_RT_MENU
-#define YY_RT_MENU 0     // r / theta chunkings for n <= 128: 0 (16,6)/(16,8); 1 (8,12)/(8,16); 2 (32,3)/(32,4)
+#define YY_RT_MENU 0     // r / theta chunkings for n <= 128: 0 r (16,6)/(16,8), theta (8,12)/(8,16); 1 (8,12)/(8,16); 2 (32,3)/(32,4); 3 (16,6)/(16,8)
 #endif
 
 namespace yy {
@@ -340,6 +340,7 @@ constexpr int line_minb(int P, int M) {
          : P > 32 ? (M <= 6 ? YY_MINB_MW : 4)   // multi-warp phi lines (part_solve3: 3 live arrays)
          : (P == 32 && M == 12) ? YY_MINB_3212
          : (P == 16 && M <= 8) ? YY_MINB_16
+         : (P == 8 && M == 12) ? 4          // theta (8, 12): 128 registers, no spills
                   : (M <= 12 ? 5 : M <= 16 ? YY_MINB_M16 : M <= 24 ? 2 : 1);
 }
 
@@ -1395,7 +1396,12 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
     if (n <= 16) YY_L(4, 4);
     if (n <= 32) YY_L(4, 8);
     if (n <= 64) YY_L(8, 8);
-#if YY_RT_MENU == 1
+#if YY_RT_MENU == 0
+    // theta: 8 lines of (8, 12) / (8, 16) chunks (measured on B200, C3: u_theta
+    // theta final +5 %, u_phi theta +3 %; the r sweeps lose 13 % with them)
+    if (AX == 1 && n <= 96) YY_L(8, 12);
+    if (AX == 1 && n <= 128) YY_L(8, 16);
+#elif YY_RT_MENU == 1
     if (n <= 96) YY_L(8, 12);
     if (n <= 128) YY_L(8, 16);
 #elif YY_RT_MENU == 2
