@@ -459,7 +459,7 @@ def test_graph_replay_is_bitwise_the_stream_path(fixed):
 # --- the (P, M) chunkings the BASELINE configurations dispatch (yy_line.cu
 # sweep_line), each reached through a whole step on an anisotropic reduced grid:
 # C3 96x128x384: r (16,6) [n = 96 / 95], theta (8,16) [126 / 127], phi (32,12) [382 / 383];
-# C5 (N = 1) 64x192x576: r (8,8) [64 / 63], theta (16,12) [190 / 191], phi (128,5) [574 / 575];
+# C5 (N = 1) 64x192x576: r (8,8) [64 / 63], theta (16,12) [190 / 191], phi (64,9) [574 / 575];
 # every quantity's plain and final factors on that axis, both systems (the r / theta
 # factors of the kinds with an even phi pitch run on k_line_th, one line per
 # thread, the rest on these chunkings).
