@@ -82,6 +82,7 @@ struct SweepArgs {
   int rev;                   // run the grid's blocks in reverse linear order (bidx)
   int noadv;                 // IMEX (YY_ADVECTION = 1): rows without transport terms — the
                              // per-step row weights are not read (16 B per element, 24 final)
+  int flat;                  // k_line_th: r boxes over the (theta, phi) plane (odd phi pitch; set by its launcher)
 };
 
 // one r-line's slab-coupling solution (yy_slab.cu)

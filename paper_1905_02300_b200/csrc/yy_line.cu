@@ -983,14 +983,18 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   double* Sx = Sc + SA;                               // u_theta reaction (RXR)
   __shared__ __align__(8) uint64_t bar[8];            // <= 8 chunks
   const int lane = threadIdx.x;
-  const int k0 = B.x * 32;                            // even: 16-B box origin
-  const int k = k0 + lane;
-  const bool valid = k >= 1 && k <= NPk(g, K) - 2;
-  const int kk = min(max(k, 1), NPk(g, K) - 2);
   int i0, j0;
   if (AX == 0) { i0 = i_lo<K>(g); j0 = B.y + 1; }
   else { i0 = B.y + i_lo<K>(g); j0 = 1; }
-  const int c1 = j0, c2 = patch * NRk(g, K) + i0;
+  // box origin (phi, theta, patch-folded r).  FLAT (r lines of a kind whose phi
+  // pitch is odd): the map's inner dimension is the whole (theta, phi) plane, the
+  // tile starts at an odd k on odd-parity rows so that the box origin stays on a
+  // 16-B boundary
+  const int k0 = B.x * 32 + (a.flat ? (j0 * NPk(g, K)) & 1 : 0);
+  const int k = k0 + lane;
+  const bool valid = k >= 1 && k <= NPk(g, K) - 2;
+  const int kk = min(max(k, 1), NPk(g, K) - 2);
+  const int c0 = a.flat ? j0 * NPk(g, K) + k0 : k0, c1 = a.flat ? 0 : j0, c2 = patch * NRk(g, K) + i0;
   // rows of this lane's line: element m at Rl + m rs (Rl clamped to a valid node)
   const int rs = (AX == 0) ? SR<K>(g) : ST<K>(g);
   const long long lofs = patch * psize(g, K) + IX<K>(g, i0, j0, kk);
@@ -1006,13 +1010,13 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
                    : "memory");
       const int o = c * TH_RC * 32;
       const int r1 = AX == 1 ? c1 + c * TH_RC : c1, r2 = AX == 0 ? c2 + c * TH_RC : c2;
-      tma_load_3d(Sd + o, &maps.m[0], &bar[c], k0, r1, r2);
+      tma_load_3d(Sd + o, &maps.m[0], &bar[c], c0, r1, r2);
       if (!a.noadv) {
-        tma_load_3d(Sc + o, &maps.m[1], &bar[c], k0, r1, r2);
-        if (RXR) tma_load_3d(Sx + o, &maps.m[2], &bar[c], k0, r1, r2);
+        tma_load_3d(Sc + o, &maps.m[1], &bar[c], c0, r1, r2);
+        if (RXR) tma_load_3d(Sx + o, &maps.m[2], &bar[c], c0, r1, r2);
       }
     }
-    if (FINAL) tma_prefetch_3d(&maps.m[3], k0, c1, c2);
+    if (FINAL) tma_prefetch_3d(&maps.m[3], c0, c1, c2);
   }
   __syncwarp();
   const double th = 0.5 * g.tau;
@@ -1160,18 +1164,20 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
 #pragma unroll
       for (int u = GB - 1; u >= 0; --u) {
         x = fma(-cv[u], x, dv[u]);
-        if (AX == 1) {
+        if (AX == 1 || a.flat) {
           if (valid && m0 + u < n) Rm[u * rs] = x;
         } else if (valid) {
           Sd[(m0 + u) * 32 + lane] = x;
         }
       }
     }
-    if (AX == 0) {
+    // (a flat box may run into the next theta row, which another block updates:
+    // flat tiles store lane by lane)
+    if (AX == 0 && !a.flat) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        tma_store_3d(&maps.m[3], Sd, k0, c1, c2);
+        tma_store_3d(&maps.m[3], Sd, c0, c1, c2);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
@@ -1225,7 +1231,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
 // host: a 3-D tensor map over every patch of one kind-K array (dims phi, theta,
 // patch-folded r), box = one tile (NL lines x n rows along AX)
 inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, int K, int npatch, int AX, int NL,
-                            int n) {
+                            int n, bool flat = false) {
   // resolved once (thread-safe static initialisation); no libcuda link dependency
   static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* fn = nullptr;
@@ -1235,8 +1241,11 @@ inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, 
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
   if (!enc) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)NPk(g, K), (cuuint64_t)NTk(g, K), (cuuint64_t)NRk(g, K) * npatch};
-  const cuuint64_t strides[2] = {(cuuint64_t)NPk(g, K) * 8, (cuuint64_t)NTk(g, K) * NPk(g, K) * 8};
+  // flat (r boxes only): dims (theta x phi plane, 1, patch-folded r)
+  const cuuint64_t plane = (cuuint64_t)NTk(g, K) * NPk(g, K);
+  const cuuint64_t dims[3] = {flat ? plane : (cuuint64_t)NPk(g, K), flat ? 1 : (cuuint64_t)NTk(g, K),
+                              (cuuint64_t)NRk(g, K) * npatch};
+  const cuuint64_t strides[2] = {flat ? plane * 8 : (cuuint64_t)NPk(g, K) * 8, plane * 8};
   const cuuint32_t box[3] = {(cuuint32_t)NL, (cuuint32_t)(AX == 1 ? n : 1), (cuuint32_t)(AX == 0 ? n : 1)};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
@@ -1283,7 +1292,9 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   const int nch = (n + TH_RC - 1) / TH_RC;
   // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
   // kinds loses to k_line, 2.0 vs 3.1 TB/s)
-  if ((NPk(g, K) % 2) || n > 256 || nch > 8) return -1;
+  // an odd phi pitch: r boxes over the whole (theta, phi) plane (its size even)
+  const bool flat = (NPk(g, K) % 2) != 0;
+  if ((flat && (AX != 0 || ((long long)NTk(g, K) * NPk(g, K)) % 2)) || n > 256 || nch > 8) return -1;
   const size_t smem =
       ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + 3 * n + (FINAL ? n : 0)) * sizeof(double);
   // measured on B200: two blocks per SM (C5 theta, 96 KB tiles) still beat the
@@ -1292,18 +1303,21 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (FINAL:
   // psi, prefetched into L2; PLAIN r: the right-hand side array, stored)
   TmaMaps maps{};
-  bool ok = encode_tile_map(&maps.m[0], a.R, g, K, npatch, AX, 32, TH_RC) &&
-            encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, TH_RC);
-  if (ok && (FINAL || AX == 0)) ok = encode_tile_map(&maps.m[3], FINAL ? a.psi : a.R, g, K, npatch, AX, 32, n);
+  bool ok = encode_tile_map(&maps.m[0], a.R, g, K, npatch, AX, 32, TH_RC, flat) &&
+            encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, TH_RC, flat);
+  if (ok && (FINAL || AX == 0))
+    ok = encode_tile_map(&maps.m[3], FINAL ? a.psi : a.R, g, K, npatch, AX, 32, n, flat);
   if (ok && Q == QUT && AX == 1) ok = encode_tile_map(&maps.m[2], a.rt, g, K, npatch, AX, 32, TH_RC);
   if (!ok) return -1;
+  SweepArgs af = a;
+  af.flat = flat;
   static size_t attr = 0;          // the largest opted-in size
   if (smem > attr) {
     cudaFuncSetAttribute(k_line_th<Q, AX, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
   const dim3 grid((NPk(g, K) + 31) / 32, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
-  k_line_th<Q, AX, MODE><<<grid, 32, smem, st>>>(g, a, maps);
+  k_line_th<Q, AX, MODE><<<grid, 32, smem, st>>>(g, af, maps);
   return (int)(grid.x * grid.y);
 }
 
