@@ -37,6 +37,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include "yy_dev.cuh"
@@ -58,6 +60,23 @@ namespace yy {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// Opt kernel `kern` into `smem` bytes of dynamic shared memory.  The opted-in
+// size of one kernel only grows and is set under a lock, so contexts on several
+// host threads (yy.h) never lower it under each other's launches.
+// (one instantiation, hence one pair of statics, per kernel: the kernel is the
+// template argument, not a function-pointer type that instantiations share)
+template <auto kern>
+inline void opt_in_smem(size_t smem) {
+  static std::atomic<size_t> cur{48 * 1024};
+  static std::mutex mu;
+  if (smem <= cur.load(std::memory_order_acquire)) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (smem > cur.load(std::memory_order_relaxed)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cur.store(smem, std::memory_order_release);
+  }
+}
 
 // Steps 2-4 on registers: rows lo_t x_{t-1} + x_t + up_t x_{t+1} = rh_t of this
 // thread's chunk c (0..P-1) of its line.  On exit rh[t] = x_t.
@@ -1311,11 +1330,7 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   if (!ok) return -1;
   SweepArgs af = a;
   af.flat = flat;
-  static size_t attr = 0;          // the largest opted-in size
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_line_th<Q, AX, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  opt_in_smem<k_line_th<Q, AX, MODE>>(smem);
   const dim3 grid((NPk(g, K) + 31) / 32, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
   k_line_th<Q, AX, MODE><<<grid, 32, smem, st>>>(g, af, maps);
   return (int)(grid.x * grid.y);
@@ -1340,11 +1355,7 @@ int launch_tma(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int TILE = 3 * NL * line_pitch<P, (M | 1)>();
   constexpr int FRONT = (NIN * SA > TILE ? NIN * SA : TILE + 15) / 16 * 16;
   const size_t smem = ((size_t)FRONT + SA + 4 * P * M) * sizeof(double);   // + row table, norm weights
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_line_tma<Q, AX, MODE, P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  opt_in_smem<k_line_tma<Q, AX, MODE, P, M>>(smem);
   const dim3 grid((NPk(g, K) - 1 + NL - 1) / NL, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
   k_line_tma<Q, AX, MODE, P, M><<<grid, 128, smem, st>>>(g, a, maps);
   return (int)(grid.x * grid.y);
@@ -1377,11 +1388,7 @@ int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatc
   // a slab line continued by the slab above must fill its chunks exactly (part_solve3)
   if (MODE == MODE_SLAB && !g.wall_hi && P * M != i_hi<K>(g) - i_lo<K>(g) + 1) return -2;
   const size_t smem = (size_t)3 * NL * line_pitch<P, (M | 1)>() * sizeof(double);
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(k_line<Q, AX, MODE, S, P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  opt_in_smem<k_line<Q, AX, MODE, S, P, M>>(smem);
   dim3 grid;
   if (AX == 2) {
     const int nlines = (i_hi<K>(g) - i_lo<K>(g) + 1) * (NTk(g, K) - 2);
