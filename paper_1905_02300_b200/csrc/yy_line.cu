@@ -1274,32 +1274,29 @@ inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, 
 
 // env YY_TMA (default 1): theta plain and final sweeps of the TMA-eligible kinds on k_line_tma
 inline bool use_tma() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = getenv("YY_TMA");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 // env YY_THOMAS (default 1): r / theta plain and final sweeps of the TMA-eligible
 // kinds on k_line_th (one line per thread)
 inline bool use_thomas() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {                         // thread-safe static initialisation
     const char* e = getenv("YY_THOMAS");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 // env YY_TH_SMEM (KB, default 110): the largest k_line_th tile
 inline int th_smem_max() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("YY_TH_SMEM");
-    v = e ? atoi(e) : 110;
-  }
+    return e ? atoi(e) : 110;
+  }();
   return v;
 }
 
