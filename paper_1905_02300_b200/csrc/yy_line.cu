@@ -51,6 +51,9 @@
 #ifndef YY_IMEX_FAST
 #define YY_IMEX_FAST 1   // IMEX rows without the per-step weight reads (0: IMEX reads the zero arrays)
 #endif
+#ifndef YY_PH384
+#define YY_PH384 0       // phi lines of 257-384 rows: 0 (32, 12); 1 (64, 6); 2 (128, 3) (tuning)
+#endif
 #ifndef YY_RT_MENU
 #define YY_RT_MENU 0     // r / theta chunkings for n <= 128: 0 r (16,6)/(16,8), theta (8,12)/(8,16); 1 (8,12)/(8,16); 2 (32,3)/(32,4); 3 (16,6)/(16,8)
 #endif
@@ -983,19 +986,28 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                ::"l"(map), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
-template <int Q, int AX, int MODE>
+// PAIR (theta lines of a kind whose phi pitch is odd, plain factor, no reaction
+// array): the tensor maps see the (theta, phi) plane as rows of theta PAIRS
+// (pitch 2 NP, a multiple of 16 B); a 32-row chunk arrives as two boxes, the 16
+// odd-theta rows (inner origin NP + k0 - 1: 34 wide, the lane's value at +1) and
+// the 16 even-theta rows (origin k0, 32 wide), PAIR_CH doubles per chunk
+constexpr int PAIR_ODD = 16 * 34, PAIR_CH = PAIR_ODD + 16 * 32;
+
+template <int Q, int AX, int MODE, bool PAIR = false>
 __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(AX != 2 && (MODE == MODE_PLAIN || MODE == MODE_FINAL), "r / theta plain or final sweeps");
+  static_assert(!PAIR || (AX == 1 && MODE == MODE_PLAIN && !(Q == QUT && AX == 1)), "pair tiles: theta, plain, no reaction");
   const uint3 B = bidx(a.rev);
   constexpr bool FINAL = (MODE == MODE_FINAL);
   constexpr bool RXR = (Q == QUT && AX == 1);
   constexpr int K = kind_of(Q);
   constexpr int G = TH_G;
+  static_assert(!PAIR || G % 2 == 0, "pair tiles: row parity from the group offset");
   const int patch = B.z;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
   const int nch = (n + TH_RC - 1) / TH_RC;
   const int NPAD = nch * TH_RC;
-  const int SA = NPAD * 32;                           // one staged array (doubles)
+  const int SA = nch * (PAIR ? PAIR_CH : TH_RC * 32);  // one staged array (doubles)
   extern __shared__ __align__(128) double sm[];
   double* Sd = sm;                                    // rhs -> d' -> x
   double* Sc = Sd + SA;                               // Astar::av -> c'
@@ -1023,10 +1035,22 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // IMEX (noadv): the rows carry no transport terms, only the rhs is staged
     const int NIN = a.noadv ? 1 : 2 + (RXR ? 1 : 0);
-    const uint32_t cb = (uint32_t)(TH_RC * 32 * sizeof(double));
+    const uint32_t cb = (uint32_t)((PAIR ? PAIR_CH : TH_RC * 32) * sizeof(double));
     for (int c = 0; c < nch; ++c) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[c])), "r"(NIN * cb)
                    : "memory");
+      if constexpr (PAIR) {
+        // rows j0 + 32 c + u: u even -> theta pair (j0 - 1) / 2 + 16 c + u / 2 at
+        // inner NP + k; u odd -> pair (j0 + 1) / 2 + 16 c + (u - 1) / 2 at inner k
+        const int o = c * PAIR_CH, t0 = (j0 - 1) / 2 + 16 * c;
+        tma_load_3d(Sd + o, &maps.m[0], &bar[c], NPk(g, K) + k0 - 1, t0, c2);
+        tma_load_3d(Sd + o + PAIR_ODD, &maps.m[2], &bar[c], k0, t0 + 1, c2);
+        if (!a.noadv) {
+          tma_load_3d(Sc + o, &maps.m[1], &bar[c], NPk(g, K) + k0 - 1, t0, c2);
+          tma_load_3d(Sc + o + PAIR_ODD, &maps.m[3], &bar[c], k0, t0 + 1, c2);
+        }
+        continue;
+      }
       const int o = c * TH_RC * 32;
       const int r1 = AX == 1 ? c1 + c * TH_RC : c1, r2 = AX == 0 ? c2 + c * TH_RC : c2;
       tma_load_3d(Sd + o, &maps.m[0], &bar[c], c0, r1, r2);
@@ -1043,6 +1067,16 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n"
         ::"r"(smem_u32(&bar[c])) : "memory");
+  };
+  // staged index of row m0 + u of this lane's line (m0 a multiple of 16, u < 16:
+  // the parity of the row is u's)
+  auto qidx = [&](int m0, int u) {
+    if constexpr (PAIR) {
+      const int base = (m0 >> 5) * PAIR_CH, h = (m0 & 31) >> 1;
+      return (u & 1) ? base + PAIR_ODD + (h + (u >> 1)) * 32 + lane : base + (h + (u >> 1)) * 34 + 1 + lane;
+    } else {
+      return (m0 + u) * 32 + lane;
+    }
   };
   // Forward elimination of the raw rows  a_m x_{m-1} + b_m x_m + c_m x_{m+1} = d_m
   // through the continuants (leading principal minors)
@@ -1093,7 +1127,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
 #pragma unroll
     for (int u = 0; u < G; ++u) {
       const int m = m0 + u, mm = EDGE ? min(m, n - 1) : m;
-      const int q = m * 32 + lane;
+      const int q = qidx(m0, u);
       // the row's a*-independent part from Geo::tsplit (staged: a broadcast read),
       // the transport weight Astar::av and the u_theta reaction from the tile
       double lo = St[3 * mm], bm = St[3 * mm + 1], up = St[3 * mm + 2];
@@ -1133,7 +1167,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     }
 #pragma unroll
     for (int u = 0; u < G; ++u) {
-      const int q = (m0 + u) * 32 + lane;
+      const int q = qidx(m0, u);
       const double inv = (u ? qv[u - 1] : q0) * frcp(qv[u]);
       dp = fma(-(ra[u] * inv), dp, rd[u] * inv);
       if (valid) {
@@ -1172,7 +1206,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
       double cv[GB], dv[GB];
 #pragma unroll
       for (int u = 0; u < GB; ++u) {
-        const int q = (m0 + u) * 32 + lane;
+        const int q = qidx(m0, u);
         cv[u] = Sc[q];
         dv[u] = Sd[q];
       }
@@ -1250,7 +1284,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
 // host: a 3-D tensor map over every patch of one kind-K array (dims phi, theta,
 // patch-folded r), box = one tile (NL lines x n rows along AX)
 inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, int K, int npatch, int AX, int NL,
-                            int n, bool flat = false) {
+                            int n, bool flat = false, int pair = 0) {
   // resolved once (thread-safe static initialisation); no libcuda link dependency
   static const PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* fn = nullptr;
@@ -1262,10 +1296,15 @@ inline bool encode_tile_map(CUtensorMap* map, const double* base, const Geo& g, 
   if (!enc) return false;
   // flat (r boxes only): dims (theta x phi plane, 1, patch-folded r)
   const cuuint64_t plane = (cuuint64_t)NTk(g, K) * NPk(g, K);
-  const cuuint64_t dims[3] = {flat ? plane : (cuuint64_t)NPk(g, K), flat ? 1 : (cuuint64_t)NTk(g, K),
+  // pair (theta boxes of an odd phi pitch, NTk even): dims (2 NP, NT / 2, patch-folded
+  // r), box (pair, n) with pair = 34 (odd-theta rows) or 32 (even-theta rows)
+  const cuuint64_t dims[3] = {pair ? 2 * (cuuint64_t)NPk(g, K) : flat ? plane : (cuuint64_t)NPk(g, K),
+                              pair ? (cuuint64_t)NTk(g, K) / 2 : flat ? 1 : (cuuint64_t)NTk(g, K),
                               (cuuint64_t)NRk(g, K) * npatch};
-  const cuuint64_t strides[2] = {flat ? plane * 8 : (cuuint64_t)NPk(g, K) * 8, plane * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)NL, (cuuint32_t)(AX == 1 ? n : 1), (cuuint32_t)(AX == 0 ? n : 1)};
+  const cuuint64_t strides[2] = {pair ? 2 * (cuuint64_t)NPk(g, K) * 8 : flat ? plane * 8 : (cuuint64_t)NPk(g, K) * 8,
+                                 plane * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)(pair ? pair : NL), (cuuint32_t)(AX == 1 ? n : 1),
+                             (cuuint32_t)(AX == 0 ? n : 1)};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1291,6 +1330,16 @@ inline bool use_thomas() {
   return v;
 }
 
+// env YY_PAIR (default 1): plain theta sweeps of an odd-phi-pitch kind (u_phi) on
+// k_line_th with theta-pair boxes
+inline bool use_pair() {
+  static const bool v = [] {
+    const char* e = getenv("YY_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // env YY_TH_SMEM (KB, default 110): the largest k_line_th tile
 inline int th_smem_max() {
   static const int v = [] {
@@ -1308,17 +1357,36 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   const int nch = (n + TH_RC - 1) / TH_RC;
   // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
   // kinds loses to k_line, 2.0 vs 3.1 TB/s)
-  // an odd phi pitch: r boxes over the whole (theta, phi) plane (its size even)
-  const bool flat = (NPk(g, K) % 2) != 0;
-  if ((flat && (AX != 0 || ((long long)NTk(g, K) * NPk(g, K)) % 2)) || n > 256 || nch > 8) return -1;
+  // an odd phi pitch: r boxes over the whole (theta, phi) plane (its size even),
+  // plain theta sweeps on theta-pair boxes (NTk even)
+  const bool odd = (NPk(g, K) % 2) != 0;
+  constexpr bool PAIR_OK = AX == 1 && MODE == MODE_PLAIN && !(Q == QUT);
+  const bool pair = odd && AX == 1;
+  const bool flat = odd && AX == 0;
+  if (pair && (!PAIR_OK || NTk(g, K) % 2 || !use_pair())) return -1;
+  if ((flat && ((long long)NTk(g, K) * NPk(g, K)) % 2) || n > 256 || nch > 8) return -1;
   const size_t smem =
-      ((size_t)nch * TH_RC * 32 * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + 3 * n + (FINAL ? n : 0)) * sizeof(double);
+      ((size_t)nch * (pair ? PAIR_CH : TH_RC * 32) * (2 + ((Q == QUT && AX == 1) ? 1 : 0)) + 3 * n +
+       (FINAL ? n : 0)) * sizeof(double);
   // measured on B200: two blocks per SM (C5 theta, 96 KB tiles) still beat the
   // partitioned k_line (3.1-3.3 vs 2.6-2.7 TB/s); one does not
   if (smem > (size_t)th_smem_max() * 1024) return -1;
   // m[0..2]: chunk boxes of the inputs; m[3]: the n-row box of the output (FINAL:
   // psi, prefetched into L2; PLAIN r: the right-hand side array, stored)
   TmaMaps maps{};
+  if constexpr (PAIR_OK) {
+    if (pair) {   // m[0], m[1]: odd-theta boxes of R, Astar::av; m[2], m[3]: even-theta boxes
+      const bool okp = encode_tile_map(&maps.m[0], a.R, g, K, npatch, AX, 32, 16, false, 34) &&
+                       encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, 16, false, 34) &&
+                       encode_tile_map(&maps.m[2], a.R, g, K, npatch, AX, 32, 16, false, 32) &&
+                       encode_tile_map(&maps.m[3], g.adv[K][AX], g, K, npatch, AX, 32, 16, false, 32);
+      if (!okp || smem > (size_t)th_smem_max() * 1024) return -1;
+      opt_in_smem<k_line_th<Q, AX, MODE, true>>(smem);
+      const dim3 grid((NPk(g, K) + 31) / 32, i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
+      k_line_th<Q, AX, MODE, true><<<grid, 32, smem, st>>>(g, a, maps);
+      return (int)(grid.x * grid.y);
+    }
+  }
   bool ok = encode_tile_map(&maps.m[0], a.R, g, K, npatch, AX, 32, TH_RC, flat) &&
             encode_tile_map(&maps.m[1], g.adv[K][AX], g, K, npatch, AX, 32, TH_RC, flat);
   if (ok && (FINAL || AX == 0))
@@ -1405,6 +1473,11 @@ int sweep_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatch
     const int n = NPk(g, K) - 2;
     if (n <= 128) YY_L(32, 4);
     if (n <= 256) YY_L(32, 8);
+#if YY_PH384 == 1
+    if (n <= 384) YY_L(64, 6);
+#elif YY_PH384 == 2
+    if (n <= 384) YY_L(128, 3);
+#endif
     if (n <= 384) YY_L(32, 12);
     if (n <= 512) YY_L(128, 4);                    // longer lines: 4 warps per line
     if (n <= 576) YY_L(64, 9);                     // two warps per line (measured on B200, C5: +23-32 % over (128, 5))

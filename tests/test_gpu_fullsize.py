@@ -29,7 +29,7 @@ def _shell(cfg, **kw):
 GOLDEN_CASES = [("C2", 1, ""), ("C3", 1, ""), ("C5", 1, ""), ("C3", 3, ""), ("C2", 5, ""), ("C2", 100, ""),
                 # the BASELINE workloads' chi = 16 (DESIGN.md RD-E4), as bench.py runs them
                 ("C2", 1, "_chi16"), ("C2", 5, "_chi16"), ("C2", 100, "_chi16"), ("C2", 200, "_chi16"),
-                ("C3", 1, "_chi16"), ("C3", 3, "_chi16"), ("C3", 5, "_chi16"), ("C3", 10, "_chi16"),
+                ("C3", 1, "_chi16"), ("C3", 3, "_chi16"), ("C3", 5, "_chi16"), ("C3", 7, "_chi16"), ("C3", 10, "_chi16"),
                 ("C5", 1, "_chi16"), ("C5", 3, "_chi16")]
 
 
