@@ -465,6 +465,7 @@ def run_yy_dist(args, rank, world, local):
     time.sleep(0.3)
     torch.cuda.synchronize()
     td.barrier()
+    l0 = sh.launch_count()
     ev0.record(stream)
     sh.step(args.steps, cfg.tol)
     ev1.record(stream)
@@ -475,6 +476,9 @@ def run_yy_dist(args, rank, world, local):
     ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
     td.all_reduce(ms, op=td.ReduceOp.MAX)
     ms = float(ms.item())
+    nl = torch.tensor([sh.launch_count() - l0], device="cuda", dtype=torch.int64)
+    td.all_reduce(nl, op=td.ReduceOp.SUM)
+    launches = int(nl.item())
     Ks = [k for k, _ in sh.stats()[-args.steps:]]
     forced = len(wl["patches"][0]["sources"]) > 0
     model_bytes = sum(step_model_bytes(cfg, k, forced) for k in Ks)
@@ -490,6 +494,14 @@ def run_yy_dist(args, rank, world, local):
                          "step_roofline": {"model": "SURVEY M1 bytes/cell = %d + 1320 K" % (352 if forced else 256),
                                            "frac_of_8TBs_per_gpu": model_bytes / (world * HBM_NOMINAL_GBS * 1e9)
                                            / (ms / 1e3)}},
+              # the step as a whole against the HBM peak of all ranks (the per-class
+              # roofline of the dominant kernel is the N = 1 line's)
+              "roofline": {"bound": "hbm", "kernel": "whole step (all ranks)",
+                           "achieved": model_bytes / (ms / 1e3) / 1e9, "peak": world * measured_peak()[0],
+                           "unit": "GB/s", "frac": model_bytes / (ms / 1e3) / 1e9 / (world * measured_peak()[0]),
+                           "traffic": None},
+              "gpu_launches": launches,
+              "e2e": None, "cpu_baseline": None,   # measured at N = 1 only (host-buffer round trip, oracle)
               "clocks": clocks, "timing": "CUDA events on each rank's stream, max over ranks"})
     sh.close()
     td.destroy_process_group()

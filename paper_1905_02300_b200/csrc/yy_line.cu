@@ -952,7 +952,8 @@ __global__ void __launch_bounds__(128, line_minb(P, M)) k_line_tma(Geo g, SweepA
 
 // ---------------------------------------------------------------------------------
 // r and theta sweeps, one line per thread (Thomas), in place in shared memory.
-// A block is ONE warp and owns 32 consecutive k-lines of one (j | i, patch): the
+// A block is ONE warp (TWO: two warps, one per end of the lines, see the kernel)
+// and owns 32 consecutive k-lines of one (j | i, patch): the
 // tile's inputs arrive by cp.async.bulk.tensor as [row][line] boxes (256-B rows)
 // in TH_RC-row chunks (one mbarrier each, so the elimination starts on the first
 // chunk while the others are in flight); lane k eliminates its line top-down,
@@ -972,7 +973,16 @@ constexpr int TH_RC = 32;         // rows per load chunk (box rows)
 // eligible one except the u_theta theta final factor (three staged arrays: two
 // blocks per SM), which keeps k_line_tma
 __host__ __device__ constexpr bool th_route(int Q, int AX, int MODE) {
-  return AX != 2 && (MODE == 0 || MODE == 2) && !(Q == QUT && AX == 1 && MODE == 2);
+  return AX != 2 && (MODE == 0 || MODE == 2);
+}
+// the u_theta theta final factor (three staged arrays) on k_line_th: env YY_TH_UTF
+// (default 0: k_line_tma)
+inline bool use_th_utf() {
+  static const bool v = [] {
+    const char* e = getenv("YY_TH_UTF");
+    return e && e[0] == '1';
+  }();
+  return v;
 }
 #ifndef YY_TH_G
 #define YY_TH_G 16
@@ -993,8 +1003,13 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
 // the 16 even-theta rows (origin k0, 32 wide), PAIR_CH doubles per chunk
 constexpr int PAIR_ODD = 16 * 34, PAIR_CH = PAIR_ODD + 16 * 32;
 
-template <int Q, int AX, int MODE, bool PAIR = false>
-__global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid_constant__ TmaMaps maps) {
+// TWO (two-way elimination, "burn at both ends"): the block is two warps on the
+// same 32 lines; warp 0 eliminates rows 0 .. H0-1 top-down, warp 1 rows NPAD-1 ..
+// H0 bottom-up (the mirrored recurrence: lower and upper weights swapped), they
+// meet at the 2x2 system of rows H0-1 / H0 and back-substitute outwards.  Same
+// shared-memory footprint, twice the warps per SM, half the serial chain.
+template <int Q, int AX, int MODE, bool PAIR = false, bool TWO = false>
+__global__ void __launch_bounds__(TWO ? 64 : 32) k_line_th(Geo g, SweepArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(AX != 2 && (MODE == MODE_PLAIN || MODE == MODE_FINAL), "r / theta plain or final sweeps");
   static_assert(!PAIR || (AX == 1 && MODE == MODE_PLAIN && !(Q == QUT && AX == 1)), "pair tiles: theta, plain, no reaction");
   const uint3 B = bidx(a.rev);
@@ -1002,18 +1017,27 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   constexpr bool RXR = (Q == QUT && AX == 1);
   constexpr int K = kind_of(Q);
   constexpr int G = TH_G;
+  constexpr int NT = TWO ? 64 : 32;
   static_assert(!PAIR || G % 2 == 0, "pair tiles: row parity from the group offset");
+  static_assert(!TWO || G == 16, "two-way elimination: halves of NPAD / 2 rows in 16-row groups");
   const int patch = B.z;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
   const int nch = (n + TH_RC - 1) / TH_RC;
   const int NPAD = nch * TH_RC;
+  const int H0 = TWO ? NPAD / 2 : NPAD;               // rows [0, H0): top-down; [H0, NPAD): bottom-up
   const int SA = nch * (PAIR ? PAIR_CH : TH_RC * 32);  // one staged array (doubles)
   extern __shared__ __align__(128) double sm[];
   double* Sd = sm;                                    // rhs -> d' -> x
   double* Sc = Sd + SA;                               // Astar::av -> c'
   double* Sx = Sc + SA;                               // u_theta reaction (RXR)
   __shared__ __align__(8) uint64_t bar[8];            // <= 8 chunks
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wid = TWO ? tid >> 5 : 0;
+  auto sync_block = [&]() {
+    if constexpr (TWO) __syncthreads();
+    else __syncwarp();
+  };
   int i0, j0;
   if (AX == 0) { i0 = i_lo<K>(g); j0 = B.y + 1; }
   else { i0 = B.y + i_lo<K>(g); j0 = 1; }
@@ -1029,14 +1053,16 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   // rows of this lane's line: element m at Rl + m rs (Rl clamped to a valid node)
   const int rs = (AX == 0) ? SR<K>(g) : ST<K>(g);
   const long long lofs = patch * psize(g, K) + IX<K>(g, i0, j0, kk);
-  if (lane == 0) {
+  if (tid == 0) {
     for (int c = 0; c < nch; ++c)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[c])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // IMEX (noadv): the rows carry no transport terms, only the rhs is staged
     const int NIN = a.noadv ? 1 : 2 + (RXR ? 1 : 0);
     const uint32_t cb = (uint32_t)((PAIR ? PAIR_CH : TH_RC * 32) * sizeof(double));
-    for (int c = 0; c < nch; ++c) {
+    for (int cc = 0; cc < nch; ++cc) {
+      // TWO: the chunks from both ends inwards (each warp starts on its own end)
+      const int c = TWO ? ((cc & 1) ? nch - 1 - (cc >> 1) : (cc >> 1)) : cc;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[c])), "r"(NIN * cb)
                    : "memory");
       if constexpr (PAIR) {
@@ -1061,7 +1087,7 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     }
     if (FINAL) tma_prefetch_3d(&maps.m[3], c0, c1, c2);
   }
-  __syncwarp();
+  sync_block();
   const double th = 0.5 * g.tau;
   auto wait = [&](int c) {
     asm volatile(
@@ -1089,45 +1115,49 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
   // Row 0's lower weight meets c_{-1} = q_{-2} = d'_{-1} = 0 and needs no mask;
   // the group holding row n-1 (line end: c = 0, wall ghost) and the padding rows
   // past n (identity rows) takes the masked build (EDGE), like the first group of a
-  // wall line.
+  // wall line.  A bottom-up warp (DIR) runs the same recurrences on the mirrored
+  // rows (group offset u -> physical row m0 + G-1-u, lower and upper weights
+  // swapped); its first rows are the padding / line-end rows.
   double qm1 = 1.0, qm2 = 0.0, cprev = 0.0, dp = 0.0;
   // the factor-row table of this tile's lines (Geo::tsplit rows i0.., j0..) into
   // shared memory (measured on B200: on a par with coef_split's 1-D factor loads
   // for the plain r-rows, 3-5 % faster for the rest)
   double* St = Sx + (RXR ? SA : 0);
   {
-    // (all of a lane's loads in flight at once: <= 3 * 256 / 32 = 24 per lane; the
+    // (all of a thread's loads in flight at once: <= 3 * 256 / 32 = 24 per lane; the
     // latency overlaps the first chunk's)
     const double* __restrict__ T3 = g.tsplit[Q][AX] + 3 * (i0 * NTk(g, K) + j0);
     const int tstride = (AX == 0) ? 3 * NTk(g, K) : 3;
-    double tv[24];
+    constexpr int NLD = 768 / NT;
+    double tv[NLD];
 #pragma unroll
-    for (int t = 0; t < 24; ++t) {
-      const int e = min(lane + 32 * t, 3 * n - 1);
+    for (int t = 0; t < NLD; ++t) {
+      const int e = min(tid + NT * t, 3 * n - 1);
       tv[t] = __ldg(T3 + (e / 3) * tstride + e % 3);
     }
 #pragma unroll
-    for (int t = 0; t < 24; ++t)
-      if (lane + 32 * t < 3 * n) St[lane + 32 * t] = tv[t];
-    __syncwarp();
+    for (int t = 0; t < NLD; ++t)
+      if (tid + NT * t < 3 * n) St[tid + NT * t] = tv[t];
   }
   // FINAL: the norm weights r^2 sin(theta) of the tile's rows
   double* Sw = St + 3 * n;
   if (FINAL) {
-    for (int m = lane; m < n; m += 32) {
+    for (int m = tid; m < n; m += NT) {
       const int i = (AX == 0) ? i0 + m : i0, j = (AX == 0) ? j0 : j0 + m;
       const double r = rnode<K>(g, i);
       Sw[m] = r * r * snode<K>(g, j);
     }
-    __syncwarp();
   }
-  auto group = [&](int m0, auto edge, auto noadv) {
-    constexpr bool EDGE = decltype(edge)::value, NOADV = decltype(noadv)::value;
-    double ra[G], rb[G], rc[G], rd[G];
+  sync_block();
+  // m0: the group's lowest physical row (a multiple of G)
+  auto group = [&](int m0, auto edge, auto noadv, auto dir) {
+    constexpr bool EDGE = decltype(edge)::value, NOADV = decltype(noadv)::value, DIR = decltype(dir)::value;
+    double ra[G], rb[G], rc[G], rd[G];   // physical lower / diagonal / upper weights, rhs of the u-th row in solve order
 #pragma unroll
     for (int u = 0; u < G; ++u) {
-      const int m = m0 + u, mm = EDGE ? min(m, n - 1) : m;
-      const int q = qidx(m0, u);
+      const int up_ = DIR ? G - 1 - u : u;
+      const int m = m0 + up_, mm = EDGE ? min(m, n - 1) : m;
+      const int q = qidx(m0, up_);
       // the row's a*-independent part from Geo::tsplit (staged: a broadcast read),
       // the transport weight Astar::av and the u_theta reaction from the tile
       double lo = St[3 * mm], bm = St[3 * mm + 1], up = St[3 * mm + 2];
@@ -1143,23 +1173,27 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
       // the line's first row: antisymmetric wall ghost of the increment (RD23);
       // its last row ul: wall ghost and c = 0 (homogeneous Dirichlet increment);
       // rows past it (padding): identity rows with d = 0
-      if (AX == 0 && K != KR && m0 == 0 && g.wall_lo) rb[0] -= ra[0];
+      if (AX == 0 && K != KR && m0 == 0 && g.wall_lo) rb[DIR ? G - 1 : 0] -= ra[DIR ? G - 1 : 0];
       const int ul = n - 1 - m0;
       const bool gh = AX == 0 && K != KR && g.wall_hi;
 #pragma unroll
       for (int u = 0; u < G; ++u) {
-        if (u == ul) {
+        const int up_ = DIR ? G - 1 - u : u;
+        if (up_ == ul) {
           if (gh) rb[u] -= rc[u];
           rc[u] = 0.0;
         }
-        if (u > ul) { ra[u] = 0.0; rb[u] = 1.0; rc[u] = 0.0; rd[u] = 0.0; }
+        if (up_ > ul) { ra[u] = 0.0; rb[u] = 1.0; rc[u] = 0.0; rd[u] = 0.0; }
       }
     }
+    // in solve order: L couples row u to the row solved before it, U to the next
+    double (&L)[G] = DIR ? rc : ra;
+    double (&U)[G] = DIR ? ra : rc;
     double qv[G];
     const double q0 = qm1;
 #pragma unroll
     for (int u = 0; u < G; ++u) {
-      const double e = ra[u] * (u ? rc[u - 1] : cprev);
+      const double e = L[u] * (u ? U[u - 1] : cprev);
       const double qn = fma(rb[u], qm1, -(e * qm2));
       qv[u] = qn;
       qm2 = qm1;
@@ -1167,15 +1201,15 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     }
 #pragma unroll
     for (int u = 0; u < G; ++u) {
-      const int q = qidx(m0, u);
+      const int q = qidx(m0, DIR ? G - 1 - u : u);
       const double inv = (u ? qv[u - 1] : q0) * frcp(qv[u]);
-      dp = fma(-(ra[u] * inv), dp, rd[u] * inv);
+      dp = fma(-(L[u] * inv), dp, rd[u] * inv);
       if (valid) {
-        Sc[q] = rc[u] * inv;
+        Sc[q] = U[u] * inv;
         Sd[q] = dp;
       }
     }
-    cprev = rc[G - 1];
+    cprev = U[G - 1];
     // 2^-e of q_{m0+G-1} (exact rescaling of the two carried continuants)
     const long long eb = (__double_as_longlong(qm1) >> 52) & 0x7ff;
     const double sc = __longlong_as_double((2046LL - eb) << 52);
@@ -1183,53 +1217,80 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     qm2 *= sc;
   };
   // (IMEX, noadv: a block-uniform branch outside the unrolled rows)
-  auto forward = [&](auto noadv) {
-    for (int c = 0; c < nch; ++c) {
-      wait(c);
-      for (int m0 = c * TH_RC; m0 < (c + 1) * TH_RC; m0 += G) {
-        const bool edge = m0 + G > n - 1 || (AX == 0 && K != KR && m0 == 0 && g.wall_lo);
-        if (edge) group(m0, std::true_type{}, noadv);
-        else group(m0, std::false_type{}, noadv);
-      }
+  auto forward = [&](auto noadv, auto dir) {
+    constexpr bool DIR = decltype(dir)::value;
+    const int HL = DIR ? NPAD - H0 : H0;
+    for (int ml = 0; ml < HL; ml += G) {
+      const int m0 = DIR ? NPAD - G - ml : ml;
+      if (m0 % TH_RC == (DIR ? TH_RC - G : 0)) wait(m0 / TH_RC);
+      const bool edge = m0 + G > n - 1 || (AX == 0 && K != KR && m0 == 0 && g.wall_lo);
+      if (edge) group(m0, std::true_type{}, noadv, dir);
+      else group(m0, std::false_type{}, noadv, dir);
     }
   };
-  if (a.noadv) forward(std::true_type{});
-  else forward(std::false_type{});
+  auto forward_dir = [&](auto dir) {
+    if (a.noadv) forward(std::true_type{}, dir);
+    else forward(std::false_type{}, dir);
+  };
+  // x: the unknown next to this warp's last eliminated row (the start of its back
+  // substitution): 0 past the padded end, or from the 2x2 system at the meeting rows
+  //   x_{H0-1} + c' x_{H0} = d'   (top-down),   a'' x_{H0-1} + x_{H0} = d''   (bottom-up)
+  double x = 0.0;
+  if constexpr (TWO) {
+    if (wid) forward_dir(std::true_type{});
+    else forward_dir(std::false_type{});
+    __syncthreads();
+    const int mo = wid ? H0 : H0 - 1, mt = wid ? H0 - 1 : H0;
+    const int qo = qidx(mo & ~15, mo & 15), qt = qidx(mt & ~15, mt & 15);
+    const double co = Sc[qo], dwn = Sd[qo], ct = Sc[qt], dt = Sd[qt];
+    x = (dt - ct * dwn) / (1.0 - ct * co);
+    __syncthreads();
+  } else {
+    forward_dir(std::false_type{});
+  }
   // back substitution x_m = d'_m - c'_m x_{m+1} from the padded top (x = 0 there:
-  // the padding rows are identity rows with d = 0).  PLAIN: x over d', then one
+  // the padding rows are identity rows with d = 0) or outwards from the meeting
+  // rows (TWO).  PLAIN: x over d', then one
   // bulk tensor store.  FINAL: psi + x straight to global (coalesced 256-B rows),
   // psi loaded one group ahead from L2 (the box was prefetched at the start).
   constexpr int GB = 16;
-  double x = 0.0;
   if constexpr (!FINAL) {
-    for (int m0 = NPAD - GB; m0 >= 0; m0 -= GB) {
-      double cv[GB], dv[GB];
+    auto backward = [&](auto dir) {
+      constexpr bool DIR = decltype(dir)::value;
+      const int HL = DIR ? NPAD - H0 : H0;
+      for (int ml = HL - GB; ml >= 0; ml -= GB) {
+        const int m0 = DIR ? NPAD - GB - ml : ml;
+        double cv[GB], dv[GB];
 #pragma unroll
-      for (int u = 0; u < GB; ++u) {
-        const int q = qidx(m0, u);
-        cv[u] = Sc[q];
-        dv[u] = Sd[q];
-      }
-      // theta: x straight to global memory (coalesced 256-B rows, no bulk store to
-      // wait for before the block exits); r: x over d', then one bulk tensor store
-      // (measured on B200: each the faster for its axis)
-      double* __restrict__ Rm = a.R + lofs + (long long)m0 * rs;
+        for (int u = 0; u < GB; ++u) {
+          const int q = qidx(m0, DIR ? GB - 1 - u : u);
+          cv[u] = Sc[q];
+          dv[u] = Sd[q];
+        }
+        // theta: x straight to global memory (coalesced 256-B rows, no bulk store to
+        // wait for before the block exits); r: x over d', then one bulk tensor store
+        // (measured on B200: each the faster for its axis)
+        double* __restrict__ Rm = a.R + lofs + (long long)m0 * rs;
 #pragma unroll
-      for (int u = GB - 1; u >= 0; --u) {
-        x = fma(-cv[u], x, dv[u]);
-        if (AX == 1 || a.flat) {
-          if (valid && m0 + u < n) Rm[u * rs] = x;
-        } else if (valid) {
-          Sd[(m0 + u) * 32 + lane] = x;
+        for (int u = GB - 1; u >= 0; --u) {
+          const int up_ = DIR ? GB - 1 - u : u;
+          x = fma(-cv[u], x, dv[u]);
+          if (AX == 1 || a.flat) {
+            if (valid && m0 + up_ < n) Rm[up_ * rs] = x;
+          } else if (valid) {
+            Sd[(m0 + up_) * 32 + lane] = x;
+          }
         }
       }
-    }
+    };
+    if (wid) backward(std::true_type{});
+    else backward(std::false_type{});
     // (a flat box may run into the next theta row, which another block updates:
     // flat tiles store lane by lane)
     if (AX == 0 && !a.flat) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
+      sync_block();
+      if (tid == 0) {
         tma_store_3d(&maps.m[3], Sd, c0, c1, c2);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1241,43 +1302,60 @@ __global__ void __launch_bounds__(32) k_line_th(Geo g, SweepArgs a, const __grid
     // psi of a row group is loaded two groups ahead of its use (ping-pong
     // registers, no copies; volatile: issued where written — plain loads were sunk
     // next to their uses), the norm weights r^2 sin(theta) come from Sw
-    auto load_psi = [&](int m0, double (&dst)[GB]) {
-      const double* Pm = P + m0 * rs;
+    auto backward = [&](auto dir) {
+      constexpr bool DIR = decltype(dir)::value;
+      auto load_psi = [&](int m0, double (&dst)[GB]) {
+        const double* Pm = P + m0 * rs;
 #pragma unroll
-      for (int u = 0; u < GB; ++u) {
-        const double* pu = (m0 + u < n) ? Pm + u * rs : P;
-        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(dst[u]) : "l"(pu));
-      }
-    };
-    auto back = [&](int m0, const double (&pv)[GB]) {
-      double cv[GB], dv[GB];
-#pragma unroll
-      for (int u = 0; u < GB; ++u) {
-        const int q = (m0 + u) * 32 + lane;
-        cv[u] = Sc[q];
-        dv[u] = Sd[q];
-      }
-      double* Pm = P + m0 * rs;
-#pragma unroll
-      for (int u = GB - 1; u >= 0; --u) {
-        x = fma(-cv[u], x, dv[u]);
-        if (valid && m0 + u < n) {
-          Pm[u * rs] = pv[u] + x;
-          wsum = fma(Sw[m0 + u] * x, x, wsum);
+        for (int u = 0; u < GB; ++u) {
+          const int up_ = DIR ? GB - 1 - u : u;
+          const double* pu = (m0 + up_ < n) ? Pm + up_ * rs : P;
+          asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(dst[u]) : "l"(pu));
         }
+      };
+      auto back = [&](int m0, const double (&pv)[GB]) {
+        double cv[GB], dv[GB];
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          const int q = (m0 + (DIR ? GB - 1 - u : u)) * 32 + lane;
+          cv[u] = Sc[q];
+          dv[u] = Sd[q];
+        }
+        double* Pm = P + m0 * rs;
+#pragma unroll
+        for (int u = GB - 1; u >= 0; --u) {
+          const int up_ = DIR ? GB - 1 - u : u;
+          x = fma(-cv[u], x, dv[u]);
+          if (valid && m0 + up_ < n) {
+            Pm[up_ * rs] = pv[u] + x;
+            wsum = fma(Sw[m0 + up_] * x, x, wsum);
+          }
+        }
+      };
+      // the warp's groups in back-substitution order: t = 0 .. ng - 1
+      const int ng = (DIR ? NPAD - H0 : H0) / GB;
+      auto base = [&](int t) { return DIR ? H0 + t * GB : H0 - GB - t * GB; };
+      double pa[GB], pb[GB];
+      load_psi(base(0), pa);
+      for (int t = 0; t < ng; t += 2) {
+        if (t + 1 < ng) load_psi(base(t + 1), pb);
+        back(base(t), pa);
+        if (t + 2 < ng) load_psi(base(t + 2), pa);
+        if (t + 1 < ng) back(base(t + 1), pb);
       }
     };
-    double pa[GB], pb[GB];
-    load_psi(NPAD - GB, pa);
-    for (int m0 = NPAD - GB; m0 > 0; m0 -= 2 * GB) {   // NPAD is a multiple of 2 GB
-      load_psi(m0 - GB, pb);
-      back(m0, pa);
-      if (m0 >= 2 * GB) load_psi(m0 - 2 * GB, pa);
-      back(m0 - GB, pb);
-    }
+    if (wid) backward(std::true_type{});
+    else backward(std::false_type{});
     wsum *= g.dr * g.dth * g.dph;
     for (int o = 16; o > 0; o >>= 1) wsum += __shfl_down_sync(FULL, wsum, o);
-    if (lane == 0) a.part[(long long)patch * a.maxb + B.y * gridDim.x + B.x] = wsum;
+    if constexpr (TWO) {
+      __shared__ double sh2[2];
+      if (lane == 0) sh2[wid] = wsum;
+      __syncthreads();
+      if (tid == 0) a.part[(long long)patch * a.maxb + B.y * gridDim.x + B.x] = sh2[0] + sh2[1];
+    } else {
+      if (lane == 0) a.part[(long long)patch * a.maxb + B.y * gridDim.x + B.x] = wsum;
+    }
   }
 }
 
@@ -1349,10 +1427,23 @@ inline int th_smem_max() {
   return v;
 }
 
+// env YY_TH2 (bit mask: 1 plain r, 2 plain theta, 4 final; default 6): k_line_th as
+// two warps per tile eliminating from both ends of the lines.  Measured on B200
+// (profiles/r02_th2_ab.txt): plain theta sweeps +7-10 % (C3), +14-22 % (C5), the
+// u_r r final factor +1-4 %, plain r sweeps -6 to -15 % (short lines; they keep one warp)
+inline int th_two_mask() {
+  static const int v = [] {
+    const char* e = getenv("YY_TH2");
+    return e ? atoi(e) : 6;
+  }();
+  return v;
+}
+
 template <int Q, int AX, int MODE>
 int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   constexpr bool FINAL = (MODE == MODE_FINAL);
+  const bool two = (th_two_mask() & (FINAL ? 4 : AX == 0 ? 1 : 2)) != 0;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
   const int nch = (n + TH_RC - 1) / TH_RC;
   // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
@@ -1381,9 +1472,14 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
                        encode_tile_map(&maps.m[2], a.R, g, K, npatch, AX, 32, 16, false, 32) &&
                        encode_tile_map(&maps.m[3], g.adv[K][AX], g, K, npatch, AX, 32, 16, false, 32);
       if (!okp || smem > (size_t)th_smem_max() * 1024) return -1;
-      opt_in_smem<k_line_th<Q, AX, MODE, true>>(smem);
       const dim3 grid((NPk(g, K) + 31) / 32, i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
-      k_line_th<Q, AX, MODE, true><<<grid, 32, smem, st>>>(g, a, maps);
+      if (two) {
+        opt_in_smem<k_line_th<Q, AX, MODE, true, true>>(smem);
+        k_line_th<Q, AX, MODE, true, true><<<grid, 64, smem, st>>>(g, a, maps);
+      } else {
+        opt_in_smem<k_line_th<Q, AX, MODE, true>>(smem);
+        k_line_th<Q, AX, MODE, true><<<grid, 32, smem, st>>>(g, a, maps);
+      }
       return (int)(grid.x * grid.y);
     }
   }
@@ -1395,9 +1491,14 @@ int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   if (!ok) return -1;
   SweepArgs af = a;
   af.flat = flat;
-  opt_in_smem<k_line_th<Q, AX, MODE>>(smem);
   const dim3 grid((NPk(g, K) + 31) / 32, AX == 0 ? NTk(g, K) - 2 : i_hi<K>(g) - i_lo<K>(g) + 1, npatch);
-  k_line_th<Q, AX, MODE><<<grid, 32, smem, st>>>(g, af, maps);
+  if (two) {
+    opt_in_smem<k_line_th<Q, AX, MODE, false, true>>(smem);
+    k_line_th<Q, AX, MODE, false, true><<<grid, 64, smem, st>>>(g, af, maps);
+  } else {
+    opt_in_smem<k_line_th<Q, AX, MODE>>(smem);
+    k_line_th<Q, AX, MODE><<<grid, 32, smem, st>>>(g, af, maps);
+  }
   return (int)(grid.x * grid.y);
 }
 
@@ -1437,7 +1538,7 @@ int launch_line(const Geo& g, const SweepArgs& a, const ResidArgs& ra, int npatc
   // theta sweeps only: measured on B200 (C3) the theta classes gain 3-9 %, the r
   // sweeps lose up to 12 % (their box rows lie 393 KB apart)
   if constexpr (th_route(Q, AX, MODE) && P <= 32) {
-    if (use_thomas()) {
+    if (use_thomas() && (!(Q == QUT && AX == 1 && MODE == MODE_FINAL) || use_th_utf())) {
       const int nb = launch_th<Q, AX, MODE>(g, a, npatch, st);
       if (nb >= 0) return nb;
     }
