@@ -48,7 +48,7 @@ def row(cfg, label, bench, parity, traffic):
     keq = ("yes (every golden step)" if parity and any(k.startswith(cfg + "_chi16") for k in parity)
            else "yes (reduced sizes)")
     return (f"| {label} | {bench['n_gpus']} | {statistics.mean(Ks):.1f} | {bench['value']:.3g} | "
-            f"{100 * sr.get('frac_of_8TBs', 0):.1f} % ({100 * sr.get('frac_of_measured_hbm', 0):.1f} % of 6557 GB/s) | "
+            f"{100 * sr.get('frac_of_8TBs', 0):.1f} % ({100 * sr.get('frac_of_measured_hbm', 0):.1f} % of the measured {(bench.get('roofline') or {}).get('peak', 0):.0f} GB/s) | "
             f"{tr} | {('%.3g (%s)' % (cpu['value'], cpu['cores'])) if cpu else '—'} | {par} | {keq} |")
 
 
