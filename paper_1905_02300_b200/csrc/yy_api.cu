@@ -126,6 +126,10 @@ struct yy_ctx {
   // (fork / join on st; YY_PAR_INTERP=0: one after the other)
   cudaStream_t aux[2] = {};
   cudaEvent_t fork[3] = {};
+  // YY_DEFER_INTERP=1 (default 0: measured +-0 on B200): only T's fringe ahead of the
+  // T solve, the p / u fringes beside it, joined before the first momentum residual
+  bool defer_interp = false;
+  bool interp_pending = false;
   double* wterm[2][MAXSRC][NW] = {};
   int nw[2] = {0, 0};
   int wtf[2][MAXSRC] = {};
@@ -826,6 +830,11 @@ InterpArgs interp_args(yy_ctx* ctx) {
 yy_status iter_solve(std::vector<yy_ctx*>& cs) {
   TRY(solve_quantity(cs, QT, 1, 0));                     // O6
   for (yy_ctx* ctx : cs)
+    if (ctx->interp_pending) {                           // the p / u fringes (beside the T solve)
+      join_interp(ctx->st, ctx->fork);
+      ctx->interp_pending = false;
+    }
+  for (yy_ctx* ctx : cs)
     if (ctx->heat_only)
       for (int q = 1; q < NSLOT; ++q) ctx->nblk[q] = 0;  // no momentum / pressure slots
   for (int s = 1; s <= 2 && !cs[0]->heat_only; ++s) {    // O7 / O9
@@ -894,9 +903,14 @@ yy_status exchange_fringe(std::vector<yy_ctx*>& cs) {
   if (cs[0]->schwarz == 2) return YY_OK;
   if (!distributed(cs)) {
     yy_ctx* ctx = cs[0];
-    ProfScope ps(ctx, "interp", 3);
-    if (ctx->aux[0]) launch_interp(ctx->g, interp_args(ctx), ctx->st, ctx->aux[0], ctx->aux[1], ctx->fork);
+    // deferred join: not with the flux correction (it reads the u fringes next)
+    // or the heat-only step (no momentum solve to overlap); the per-class timing
+    // pass (prof_on) keeps the classes apart
+    const bool defer = ctx->aux[0] && ctx->defer_interp && !(ctx->flux_eps > 0) && !ctx->heat_only && !ctx->prof_on;
+    ProfScope ps(ctx, "interp", defer ? 4 : 3);
+    if (ctx->aux[0]) launch_interp(ctx->g, interp_args(ctx), ctx->st, ctx->aux[0], ctx->aux[1], ctx->fork, defer);
     else launch_interp(ctx->g, interp_args(ctx), ctx->st);
+    ctx->interp_pending = defer;
     return YY_OK;
   }
   for (yy_ctx* ctx : cs) {                                // donor side: the partner's fringe
@@ -1339,6 +1353,8 @@ yy_status create_ctx(const yy_grid* gr, double R1, double R2, double Pr, double 
   // both patches in this context (the interpolation kernels write every fringe):
   // system 2 reads p1^(k) - p1^n from one array (YY_DP1=0: off)
   const char* epi = std::getenv("YY_PAR_INTERP");
+  const char* edi = std::getenv("YY_DEFER_INTERP");
+  ctx->defer_interp = edi && edi[0] == '1';
   if (npatch == 2 && nslab == 1 && !(epi && epi[0] == '0')) {
     for (int q = 0; q < 2; ++q)
       if (cudaStreamCreateWithFlags(&ctx->aux[q], cudaStreamNonBlocking) != cudaSuccess) { yy_destroy(ctx); return YY_ECUDA; }

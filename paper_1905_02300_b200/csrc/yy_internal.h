@@ -140,6 +140,7 @@ struct InterpArgs {
   VecTab tab_th, tab_ph;
   double* dp1;               // with p1n: also write p1^(k) - p1^n at the p1 fringe (or NULL)
   const double* p1n;
+  int cc_q0, cc_nq;          // k_interp_cc: quantities cc_q0 .. cc_q0 + cc_nq - 1 (0 quantities: all 5)
 };
 
 void launch_lincomb(double* out, long long n, const LinIn& in, int nin, cudaStream_t st);
@@ -189,8 +190,12 @@ void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double
                          bool fixed, cudaStream_t st);
 // the three fringe classes (cell/r-face lattice, theta faces, phi faces); with s2,
 // s3 and ev[3] given they run concurrently (fork / join on st through the events)
+// defer: only T's fringe on st; the other four cell-lattice quantities (on s2, ahead
+// of the theta faces) and the phi faces are left running — the caller joins them
+// with join_interp before anything reads the p / u fringes (they overlap the T solve)
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st, cudaStream_t s2 = nullptr,
-                   cudaStream_t s3 = nullptr, cudaEvent_t* ev = nullptr);
+                   cudaStream_t s3 = nullptr, cudaEvent_t* ev = nullptr, bool defer = false);
+void join_interp(cudaStream_t st, cudaEvent_t* ev);
 // one patch per context: the donor evaluates the partner's fringe values from its
 // own patch into buf (pack), the target writes a received buf into its fringe
 // (unpack).  Layout: [cc: 5 x (nr+1) x n_cc][th: 2 x nr x n_th][ph: 2 x nr x n_ph].

@@ -409,7 +409,8 @@ constexpr int IL = 4;
 // grid: x -> entry, y -> group of IL r-levels (0..nr), z -> patch*5 + quantity
 __global__ void k_interp_cc(Geo g, InterpArgs a) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int patch = blockIdx.z / 5, q = blockIdx.z % 5;
+  const int nq = a.cc_nq ? a.cc_nq : 5;
+  const int patch = blockIdx.z / nq, q = a.cc_q0 + blockIdx.z % nq;
   if (e >= a.tab_cc.n) return;
   const int K = (q < 3) ? KC : KR;
   const int lo = K == KC ? g.ifr_c0 : g.ifr_f0, hi = K == KC ? g.ifr_c1 : g.ifr_f1;
@@ -786,23 +787,38 @@ void launch_schwarz_cond(cudaGraphConditionalHandle h, const double* red, double
 }
 
 void launch_interp(const Geo& g, const InterpArgs& a, cudaStream_t st, cudaStream_t s2, cudaStream_t s3,
-                   cudaEvent_t* ev) {
+                   cudaEvent_t* ev, bool defer) {
   const int ngc = (g.nr + 1 + IL - 1) / IL, ngv = (g.nr + IL - 1) / IL;
   const bool par = s2 && s3 && ev;
+  defer = defer && par;
   if (par) {
     cudaEventRecord(ev[0], st);
     cudaStreamWaitEvent(s2, ev[0], 0);
     cudaStreamWaitEvent(s3, ev[0], 0);
   }
-  if (a.tab_cc.n) k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 10), 128, 0, st>>>(g, a);
+  if (a.tab_cc.n) {
+    if (defer) {   // T alone ahead of the T solve; p1, p2, u_r1, u_r2 beside it
+      InterpArgs t = a, r = a;
+      t.cc_q0 = 0; t.cc_nq = 1;
+      r.cc_q0 = 1; r.cc_nq = 4;
+      k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 2), 128, 0, st>>>(g, t);
+      k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 8), 128, 0, s2>>>(g, r);
+    } else {
+      k_interp_cc<<<dim3((a.tab_cc.n + 127) / 128, ngc, 10), 128, 0, st>>>(g, a);
+    }
+  }
   if (a.tab_th.n) k_interp_vec<KT><<<dim3((a.tab_th.n + 127) / 128, ngv, 4), 128, 0, par ? s2 : st>>>(g, a);
   if (a.tab_ph.n) k_interp_vec<KP><<<dim3((a.tab_ph.n + 127) / 128, ngv, 4), 128, 0, par ? s3 : st>>>(g, a);
   if (par) {
     cudaEventRecord(ev[1], s2);
     cudaEventRecord(ev[2], s3);
-    cudaStreamWaitEvent(st, ev[1], 0);
-    cudaStreamWaitEvent(st, ev[2], 0);
+    if (!defer) join_interp(st, ev);
   }
+}
+
+void join_interp(cudaStream_t st, cudaEvent_t* ev) {
+  cudaStreamWaitEvent(st, ev[1], 0);
+  cudaStreamWaitEvent(st, ev[2], 0);
 }
 
 long long fringe_count(const Geo& g, const InterpArgs& a) {

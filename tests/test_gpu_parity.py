@@ -221,22 +221,28 @@ def test_line_solve_every_chunking(shape):
         assert np.array_equal(x2.cpu().numpy(), got), (shape, axis)
 
 
-@pytest.mark.parametrize("var", ["YY_ALT_ORDER", "YY_DP1"])
-def test_data_path_options_are_bitwise_neutral(var):
+@pytest.mark.parametrize("var,stream", [("YY_ALT_ORDER", False), ("YY_DP1", False),
+                                        ("YY_DEFER_INTERP", False), ("YY_DEFER_INTERP", True)])
+def test_data_path_options_are_bitwise_neutral(var, stream):
     """YY_ALT_ORDER: consecutive residual / sweep / pressure kernels run their
     blocks in alternating linear order (L2 reuse) — every block computes the same
     tile and the norm partials keep their slots.  YY_DP1: system 2 reads
     p1^(k) - p1^n from one array written by the system-1 pressure update and the
     p1 fringe interpolation instead of forming it from p1^(k) and p1^n — the same
-    subtraction.  Either way the step is bit-identical with the option off."""
+    subtraction.  YY_DEFER_INTERP: only T's fringe is interpolated ahead of the T
+    solve, the p / u fringes on side streams beside it, joined before the first
+    momentum residual (stream launches, and captured into the device-side loop
+    graph on a user stream).  Either way the step is bit-identical with the option off."""
     import os
+    import torch
     cfg = W.small("C3", 9, 17, 47)
     wl = W.random_state(cfg, seed=3, amp=1.0)
     out = []
+    st = torch.cuda.Stream() if stream else None
     for val in ("1", "0"):
         os.environ[var] = val
         try:
-            sh = _shell(cfg)
+            sh = _shell(cfg, **({"stream": st.cuda_stream} if stream else {}))
             sh.load_workload(wl)
             sh.step(2, cfg.tol)
             out.append(([sh.get_fields(p, 0, s) for p in range(2) for s in (1, 2)], sh.stats()))
