@@ -1016,10 +1016,13 @@ __global__ void __launch_bounds__(TWO ? 64 : 32) k_line_th(Geo g, SweepArgs a, c
   constexpr bool FINAL = (MODE == MODE_FINAL);
   constexpr bool RXR = (Q == QUT && AX == 1);
   constexpr int K = kind_of(Q);
-  constexpr int G = TH_G;
+  // rows per elimination group: 16 on one warp; 8 for the two-way form (measured on
+  // B200: theta plain +5-7 %, u_r r final +4.5 %, profiles/r02_th2_g8_ab.txt — half
+  // the unrolled code per direction in the instruction cache)
+  constexpr int G = TWO ? 8 : TH_G;
   constexpr int NT = TWO ? 64 : 32;
   static_assert(!PAIR || G % 2 == 0, "pair tiles: row parity from the group offset");
-  static_assert(!TWO || G == 16, "two-way elimination: halves of NPAD / 2 rows in 16-row groups");
+  static_assert(16 % G == 0, "the halves of a two-way tile (NPAD / 2 rows) and the 32-row chunks in whole groups");
   const int patch = B.z;
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
   const int nch = (n + TH_RC - 1) / TH_RC;
