@@ -1256,7 +1256,10 @@ __global__ void __launch_bounds__(TWO ? 64 : 32) k_line_th(Geo g, SweepArgs a, c
   // rows (TWO).  PLAIN: x over d', then one
   // bulk tensor store.  FINAL: psi + x straight to global (coalesced 256-B rows),
   // psi loaded one group ahead from L2 (the box was prefetched at the start).
-  constexpr int GB = 16;
+#ifndef YY_TH_GB2
+#define YY_TH_GB2 16
+#endif
+  constexpr int GB = TWO ? YY_TH_GB2 : 16;   // rows per back-substitution group
   if constexpr (!FINAL) {
     auto backward = [&](auto dir) {
       constexpr bool DIR = decltype(dir)::value;
