@@ -1256,8 +1256,10 @@ __global__ void __launch_bounds__(TWO ? 64 : 32) k_line_th(Geo g, SweepArgs a, c
   // rows (TWO).  PLAIN: x over d', then one
   // bulk tensor store.  FINAL: psi + x straight to global (coalesced 256-B rows),
   // psi loaded one group ahead from L2 (the box was prefetched at the start).
+  // (two-way: 8-row groups, like the elimination's — measured on B200: u_r r final
+  // 3.62 -> 3.96 TB/s on C3, 4.60 -> 4.88 on C5; profiles/r02_late_switches_ab.txt)
 #ifndef YY_TH_GB2
-#define YY_TH_GB2 16
+#define YY_TH_GB2 8
 #endif
   constexpr int GB = TWO ? YY_TH_GB2 : 16;   // rows per back-substitution group
   if constexpr (!FINAL) {
@@ -1433,14 +1435,17 @@ inline int th_smem_max() {
   return v;
 }
 
-// env YY_TH2 (bit mask: 1 plain r, 2 plain theta, 4 final; default 6): k_line_th as
+// env YY_TH2 (bit mask: 1 plain r, 2 plain theta, 4 final; default 7): k_line_th as
 // two warps per tile eliminating from both ends of the lines.  Measured on B200
-// (profiles/r02_th2_ab.txt): plain theta sweeps +7-10 % (C3), +14-22 % (C5), the
-// u_r r final factor +1-4 %, plain r sweeps -6 to -15 % (short lines; they keep one warp)
+// (profiles/r02_th2_ab.txt, 16-row groups): plain theta sweeps +7-10 % (C3), +14-22 %
+// (C5), the u_r r final factor +1-4 %, plain r sweeps -6 to -15 %; with 8-row groups
+// (profiles/r02_late_switches_ab.txt) the plain r sweeps of C3's 96-row lines gain
+// too (u_theta r 4.10 -> 4.61 TB/s, u_phi r 4.09 -> 4.34); lines of <= 64 rows (C5's
+// r lines: two 32-row halves) keep one warp
 inline int th_two_mask() {
   static const int v = [] {
     const char* e = getenv("YY_TH2");
-    return e ? atoi(e) : 6;
+    return e ? atoi(e) : 7;
   }();
   return v;
 }
@@ -1449,7 +1454,8 @@ template <int Q, int AX, int MODE>
 int launch_th(const Geo& g, const SweepArgs& a, int npatch, cudaStream_t st) {
   constexpr int K = kind_of(Q);
   constexpr bool FINAL = (MODE == MODE_FINAL);
-  const bool two = (th_two_mask() & (FINAL ? 4 : AX == 0 ? 1 : 2)) != 0;
+  const int n_ = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
+  const bool two = (th_two_mask() & (FINAL ? 4 : AX == 0 ? 1 : 2)) != 0 && !(!FINAL && AX == 0 && n_ <= 64);
   const int n = (AX == 0) ? i_hi<K>(g) - i_lo<K>(g) + 1 : NTk(g, K) - 2;
   const int nch = (n + TH_RC - 1) / TH_RC;
   // 16-B row pitch (tensor maps; measured: 8-B cp.async staging of the odd-pitch
